@@ -1,0 +1,218 @@
+/* gridopf.h -- C-ABI of the B200 condensed-space ACOPF solve path.
+ *
+ * One shared library (paper_2307_16830_b200/_lib/libgridopf.so) holds the
+ * host symbolic analysis (C++) and the sm_100a CUDA kernels.  Every entry
+ * point takes plain pointers and sizes; device pointers are caller-owned
+ * (allocated by the Python layer through torch) and all device work is
+ * stream-ordered on the `stream` argument (a cudaStream_t).
+ *
+ * The reference (gridnlp 0.1.0, /root/reference/pkg/src/gridnlp) has no
+ * C FFI; its boundaries are Python duck types plus two numba kernels.  Each
+ * declaration below names the reference interface it replaces.  See
+ * INTEGRATION.md for the ctypes binding a gridnlp maintainer would add.
+ *
+ * Return codes: 0 = OK, negative = error; gn_last_error() has the text.
+ * Plans are not thread-safe (one stream per plan), mirroring the
+ * reference's exclusive-use solver instances.
+ */
+#ifndef GRIDOPF_H
+#define GRIDOPF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gn_model gn_model;         /* compiled pattern-block model + AD plan */
+typedef struct gn_condense gn_condense;   /* pattern of W + I + tril(A^T A) + maps   */
+typedef struct gn_symbolic gn_symbolic;   /* ordering-dependent factor structure     */
+typedef struct gn_kkt gn_kkt;             /* KKT vector-kernel plan (A, W gathers)   */
+
+const char *gn_last_error(void);
+int gn_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Host structure (CPU; no device needed)                              */
+/* ------------------------------------------------------------------ */
+
+/* Deterministic record permutation: lexicographic on (targets,
+ * var_idx[:,0..], params[:,0..]), stable.
+ * Replaces model.py:128-140 (_canonical_order). */
+int gn_canonical_order(int64_t n_records, int32_t n_var_slots, int32_t n_param_slots,
+                       const int64_t *var_idx, const double *params,
+                       const int64_t *targets /* nullable */, int64_t *order_out);
+
+/* One pattern block = (instruction tape, data arrays).  kind: 0 objective
+ * sum, 1 constraint define, 2 constraint increment (model.py:24-26).
+ * Records must already be in canonical order. */
+typedef struct gn_block_desc {
+  int32_t kind;
+  int32_t n_var_slots, n_param_slots;
+  int64_t n_records;
+  const int64_t *var_idx;  /* [n_records][n_var_slots]   */
+  const double *params;    /* [n_records][n_param_slots] */
+  const int64_t *targets;  /* [n_records] or NULL         */
+  int32_t n_ops;           /* tape (expressions.py:126-145) */
+  const int32_t *ops;      /* [n_ops][3] = (op, a, b)       */
+  int32_t n_consts;
+  const double *consts;
+  int32_t out;
+  int32_t n_first;         /* first-derivative slots (sorted)                   */
+  const int32_t *first_slots;
+  int32_t n_pairs;         /* second-derivative pairs (a >= b), sorted          */
+  const int32_t *pairs;    /* [n_pairs][2] */
+  const int32_t *grad_order; /* [n_first] slot order of the reverse sweep (dict order) */
+} gn_block_desc;
+
+/* Expand templates over records, dedup, build slot maps and the device
+ * gather plans.  Replaces CompiledModel.__init__ (model.py:236-303). */
+int gn_model_create(const gn_block_desc *blocks, int32_t n_blocks, int64_t n_var,
+                    int64_t n_con, gn_model **out);
+int gn_model_info(const gn_model *mdl, int64_t *nnz_jac, int64_t *nnz_hess,
+                  int64_t *n_contrib);
+/* jac_slots / hess_slots / hess_factor are concatenated block by block,
+ * slot-major: block b contributes n_first*R (constraint blocks only) resp.
+ * n_pairs*R entries. */
+int gn_model_export(const gn_model *mdl, int64_t *jac_rows, int64_t *jac_cols,
+                    int64_t *hess_rows, int64_t *hess_cols, int64_t *jac_slots,
+                    int64_t *hess_slots, double *hess_factor);
+void gn_model_destroy(gn_model *mdl);
+
+/* Pattern of W + I + tril(A^T A), lower CSC, and its scatter maps.
+ * Replaces kkt.py:243-283 (symbolic_condense) + csc.py:52-76. */
+int gn_condense_create(int64_t n, int64_t nnz_h, const int64_t *hess_rows,
+                       const int64_t *hess_cols, int64_t nnz_j, const int64_t *jac_rows,
+                       const int64_t *jac_cols, gn_condense **out);
+int gn_condense_info(const gn_condense *cs, int64_t *nnz_k, int64_t *n_products);
+int gn_condense_export(const gn_condense *cs, int64_t *indptr, int64_t *indices,
+                       int64_t *w_map, int64_t *diag_map, int64_t *ata_map,
+                       int64_t *ata_row, int64_t *ata_s1, int64_t *ata_s2);
+void gn_condense_destroy(gn_condense *cs);
+
+/* Generic lower-CSC -> (CSC, slot map) conversion (csc.py:52-76).
+ * Two-phase: call with indptr_out == NULL to get *nnz_out. */
+int gn_coo_to_csc(int64_t n, int64_t nnz, const int64_t *rows, const int64_t *cols,
+                  int64_t *nnz_out, int64_t *indptr_out, int64_t *indices_out,
+                  int64_t *slot_map_out);
+
+/* Exact greedy minimum degree, key (degree, initial degree, index).
+ * Replaces amd.py:18-54 (amd_order); bit-identical permutation. */
+int gn_min_degree(int64_t n, const int64_t *indptr, const int64_t *indices,
+                  int64_t *perm_out);
+
+/* Symbolic Cholesky of the permuted pattern + the supernodal front plan.
+ * Replaces cholesky.py:56-144 (elimination_tree, _row_patterns,
+ * symbolic_cholesky). */
+int gn_symbolic_create(int64_t n, const int64_t *indptr, const int64_t *indices,
+                       const int64_t *perm, gn_symbolic **out);
+typedef struct gn_symbolic_info_t {
+  int64_t n, nnz_a, nnz_l, n_fronts, front_doubles, vec_doubles, max_front, max_cols;
+  int64_t n_levels, flops;
+} gn_symbolic_info_t;
+int gn_symbolic_info(const gn_symbolic *sym, gn_symbolic_info_t *info);
+int gn_symbolic_export(const gn_symbolic *sym, int64_t *parent, int64_t *a_rowptr,
+                       int64_t *a_rowcol, int64_t *a_srcslot, int64_t *row_ptr,
+                       int64_t *row_cols, int64_t *l_colptr, int64_t *l_rowidx);
+void gn_symbolic_destroy(gn_symbolic *sym);
+
+/* ------------------------------------------------------------------ */
+/* Device (sm_100a)                                                    */
+/* ------------------------------------------------------------------ */
+
+/* what-mask for gn_ad_eval */
+#define GN_AD_F 1u
+#define GN_AD_C 2u
+#define GN_AD_GRAD 4u
+#define GN_AD_JAC 8u
+#define GN_AD_HESS 16u
+
+int gn_model_upload(gn_model *mdl);
+/* Objective, constraints, gradient, Jacobian and Lagrangian Hessian values.
+ * Replaces autodiff.py:45-142 (eval_*), with the _Problem scaling
+ * (ipm.py:208-249) folded in: f *= obj_scale, c[i] *= con_scale[i],
+ * grad *= obj_scale, jac[k] *= con_scale[row k], Hessian weights
+ * obj_weight and y[i]*con_scale[i].  con_scale may be NULL (= 1).
+ * Non-finite results set bits of *flags (GN_AD_* of the offending
+ * output) instead of raising.  f points to ONE device double. */
+int gn_ad_eval(gn_model *mdl, const double *x, const double *y, double obj_weight,
+               const double *con_scale, double obj_scale, double *f, double *c,
+               double *grad, double *jac, double *hess, uint32_t what,
+               double *contrib_ws, int32_t *flags, void *stream);
+
+int gn_symbolic_upload(gn_symbolic *sym);
+/* Numeric refactorisation on the fixed pivot order.  kvals are the matrix
+ * values in the CSC layout given to gn_symbolic_create.  *fail_col
+ * (device int64) receives the smallest failing pivot position or n.
+ * Replaces _chol_kernel/factorize (cholesky.py:147-205). */
+int gn_chol_factor(gn_symbolic *sym, const double *kvals, double *fronts,
+                   int64_t *fail_pos, void *stream);
+/* x = P^T L^-T L^-1 P b; b and x may alias.  ws: vec_doubles scratch.
+ * Replaces _solve_kernel/solve (cholesky.py:175-217). */
+int gn_chol_solve(gn_symbolic *sym, const double *fronts, const double *b, double *x,
+                  double *ws, void *stream);
+/* Factor values in the reference CSC layout (l_colptr/l_rowidx). */
+int gn_chol_export_l(gn_symbolic *sym, const double *fronts, double *l_vals, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Condensed KKT system (device)                                       */
+/* ------------------------------------------------------------------ */
+
+/* Values of the seven-block Newton system at the current iterate
+ * (KKTWorkspace, kkt.py:96-129).  Widths are +inf for absent bounds. */
+typedef struct gn_kkt_state {
+  const double *w, *a;                   /* W lower-COO values, Jacobian values */
+  const double *dxl, *dxu, *dsl, *dsu;   /* bound widths                       */
+  const double *zxl, *zxu, *zsl, *zsu;   /* bound duals                        */
+  const double *sx, *ss;                 /* Sigma_x, Sigma_s                   */
+  double dw, dc;                         /* delta_w, delta_c                   */
+} gn_kkt_state;
+
+/* seven-block vector (PVec / Steps, kkt.py:60-85) */
+typedef struct gn_vec7 {
+  double *x, *s, *y, *zxl, *zxu, *zsl, *zsu;
+} gn_vec7;
+
+/* Gather plans for W v, A v, A^T u and the K assembly (cs may be NULL when
+ * no assembly is needed). */
+int gn_kkt_create(int64_t n, int64_t m, int64_t nnz_h, const int64_t *hess_rows,
+                  const int64_t *hess_cols, int64_t nnz_j, const int64_t *jac_rows,
+                  const int64_t *jac_cols, const gn_condense *cs, gn_kkt **out);
+void gn_kkt_destroy(gn_kkt *k);
+/* sigma = zl/dl + zu/du over finite widths (kkt.py:121-129) */
+int gn_kkt_sigma(int64_t len, const double *dl, const double *du, const double *zl,
+                 const double *zu, double *sigma, void *stream);
+/* kind 0: W v (symmetric, from the lower triangle), 1: A v, 2: A^T u
+ * (kkt.py:132-150); accumulation order = the reference's np.add.at order */
+int gn_kkt_matvec(gn_kkt *k, int kind, const double *vals, const double *v, double *out,
+                  void *stream);
+/* K = W + (Sigma_x + dw) I + A^T D A in the condensed CSC layout
+ * (CondensedBackend.assemble, kkt.py:300-312) */
+int gn_kkt_assemble(gn_kkt *k, const gn_kkt_state *st, double *kvals, void *stream);
+/* (qx, qs, qy) = condense_pvec(pv); rhs = qx + A^T (C qs + D qy)
+ * (kkt.py:159-167) */
+int gn_kkt_condense_rhs(gn_kkt *k, const gn_kkt_state *st, const gn_vec7 *pv, double *qx,
+                        double *qs, double *qy, double *rhs, void *stream);
+/* ds = C (A dx + dc qs - qy), dy = (Sigma_s + dw) ds - qs (kkt.py:169-173) */
+int gn_kkt_recover_slack_dual(gn_kkt *k, const gn_kkt_state *st, const double *dx,
+                              const double *qs, const double *qy, double *ds, double *dy,
+                              void *stream);
+/* bound-dual steps (kkt.py:175-187); sets bit 1 of *flags when a finite
+ * width is not positive (DegenerateInterior) */
+int gn_kkt_recover_bound_duals(gn_kkt *k, const gn_kkt_state *st, const double *dx,
+                               const double *ds, const gn_vec7 *pv, double *dzxl, double *dzxu,
+                               double *dzsl, double *dzsu, int32_t *flags, void *stream);
+/* res = pv - M_full * steps accumulated in double-double, rounded to
+ * double; *norm = residual_norm(res) (kkt.py:190-209, 224-229) */
+int gn_kkt_residual(gn_kkt *k, const gn_kkt_state *st, const gn_vec7 *steps,
+                    const gn_vec7 *pv, gn_vec7 *res, double *norm, void *stream);
+/* matrix_scale (kkt.py:211-221) into *out (device) */
+int gn_kkt_matrix_scale(gn_kkt *k, const gn_kkt_state *st, double *out, void *stream);
+/* y += alpha x over all seven blocks (Steps.axpy, kkt.py:83-85) */
+int gn_vec7_axpy(gn_kkt *k, gn_vec7 *y, const gn_vec7 *x, double alpha, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDOPF_H */

@@ -1,0 +1,468 @@
+// Pattern-block AD evaluator on sm_100a.
+//
+// One launch evaluates every record of every pattern block: CTA ranges map
+// to blocks, one thread per record runs the block's instruction tape
+// (forward values, reverse adjoints, forward-over-reverse Hessian columns)
+// exactly as the reference interpreter does (expressions.py:222-409,
+// including its "absent adjoint" semantics), and writes per-record
+// contributions to a fixed contribution array.  A second launch gathers
+// the contributions of every output slot (constraint rows, gradient
+// entries, Jacobian / Hessian COO slots) in the reference's np.add.at
+// order (autodiff.py:57-142): deterministic, no floating-point atomics.
+// A single-CTA kernel reduces the objective.
+#include <cmath>
+
+#include "device.cuh"
+
+namespace gn {
+namespace {
+
+constexpr int kRecThreads = 128;
+enum { OP_VAR = 0, OP_PAR, OP_CONST, OP_ADD, OP_SUB, OP_MUL, OP_DIV, OP_POW, OP_NEG, OP_SIN,
+       OP_COS, OP_LOG, OP_SQRT, OP_EXP };
+
+// numpy's scalar fast paths for array ** c (square, sqrt, reciprocal, identity)
+__device__ __forceinline__ double powc(double v, double c) {
+  if (c == 2.0) return v * v;
+  if (c == 1.0) return v;
+  if (c == 0.0) return 1.0;
+  if (c == 0.5) return sqrt(v);
+  if (c == -1.0) return 1.0 / v;
+  return pow(v, c);
+}
+
+struct Partials {
+  double fa, fb;
+  bool has_b;
+};
+
+// (d entry/d a, d entry/d b) -- expressions.py:259-285
+__device__ __forceinline__ Partials partials(int op, int a, int b, int i, const double *v,
+                                             const double *consts) {
+  switch (op) {
+    case OP_ADD: return {1.0, 1.0, true};
+    case OP_SUB: return {1.0, -1.0, true};
+    case OP_MUL: return {v[b], v[a], true};
+    case OP_DIV: return {1.0 / v[b], -v[a] / (v[b] * v[b]), true};
+    case OP_POW: { double c = consts[b]; return {c * powc(v[a], c - 1.0), 0.0, false}; }
+    case OP_NEG: return {-1.0, 0.0, false};
+    case OP_SIN: return {cos(v[a]), 0.0, false};
+    case OP_COS: return {-sin(v[a]), 0.0, false};
+    case OP_LOG: return {1.0 / v[a], 0.0, false};
+    case OP_SQRT: return {0.5 / v[i], 0.0, false};
+    default: return {v[i], 0.0, false};  // EXP
+  }
+}
+
+__device__ __forceinline__ bool is_binary(int op) { return op >= OP_ADD && op <= OP_DIV; }
+
+__device__ __forceinline__ void acc(double *arr, uint64_t &mask, int k, double val) {
+  if ((mask >> k) & 1ull) arr[k] += val;
+  else { arr[k] = val; mask |= 1ull << k; }
+}
+
+__global__ void __launch_bounds__(kRecThreads)
+ad_records_kernel(const DevBlock *__restrict__ blocks, int nblocks, const int4 *__restrict__ tape,
+                  const double *__restrict__ consts_pool, const int32_t *__restrict__ slot_pool,
+                  const int32_t *__restrict__ var_idx, const double *__restrict__ params,
+                  const int32_t *__restrict__ targets, const double *__restrict__ x,
+                  const double *__restrict__ y, const double *__restrict__ con_scale,
+                  double obj_w, uint32_t what, double *__restrict__ contrib) {
+  __shared__ DevBlock sb;
+  __shared__ int4 s_tape[kMaxTape];
+  __shared__ double s_const[kMaxTape];
+  __shared__ int32_t s_slots[kMaxSlots + 3 * kMaxSlots * (kMaxSlots + 1) / 2 + kMaxSlots];
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = nblocks - 1;
+    while (lo < hi) {  // last block with cta_begin <= blockIdx.x
+      int mid = (lo + hi + 1) >> 1;
+      if (blocks[mid].cta_begin <= static_cast<int64_t>(blockIdx.x)) lo = mid; else hi = mid - 1;
+    }
+    sb = blocks[lo];
+  }
+  __syncthreads();
+  const DevBlock &B = sb;
+  const bool obj = B.kind == 0;
+  const bool need_val = obj ? (what & GN_AD_F) : (what & GN_AD_C);
+  const bool need_first = obj ? (what & GN_AD_GRAD) : (what & GN_AD_JAC);
+  const bool need_hess = (what & GN_AD_HESS) && B.npairs > 0;
+  if (!need_val && !need_first && !need_hess) return;
+  for (int t = threadIdx.x; t < B.T; t += blockDim.x) s_tape[t] = tape[B.tape_off + t];
+  for (int t = threadIdx.x; t < B.nconst; t += blockDim.x) s_const[t] = consts_pool[B.const_off + t];
+  const int nslot = B.nfirst + 2 * B.npairs + B.nsweep;
+  for (int t = threadIdx.x; t < nslot; t += blockDim.x) s_slots[t] = slot_pool[B.slot_off + t];
+  __syncthreads();
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) - B.cta_begin) * blockDim.x + threadIdx.x;
+  if (r >= B.R) return;
+  const int *first = s_slots;
+  const int *pair_a = s_slots + B.nfirst;
+  const int *pair_b = pair_a + B.npairs;
+  const int *sweep = pair_b + B.npairs;
+  const int T = B.T;
+  const int64_t R = B.R;
+
+  double X[kMaxSlots];
+  for (int s = 0; s < B.nv; ++s) X[s] = x[var_idx[B.var_off + s * R + r]];
+  double v[kMaxTape];
+  // ---- forward (expressions.py:222-254)
+  for (int i = 0; i < T; ++i) {
+    int4 e = s_tape[i];
+    double o;
+    switch (e.x) {
+      case OP_VAR: o = X[e.y]; break;
+      case OP_PAR: o = params[B.par_off + e.y * R + r]; break;
+      case OP_CONST: o = s_const[e.z]; break;
+      case OP_ADD: o = v[e.y] + v[e.z]; break;
+      case OP_SUB: o = v[e.y] - v[e.z]; break;
+      case OP_MUL: o = v[e.y] * v[e.z]; break;
+      case OP_DIV: o = v[e.y] / v[e.z]; break;
+      case OP_POW: o = powc(v[e.y], s_const[e.z]); break;
+      case OP_NEG: o = -v[e.y]; break;
+      case OP_SIN: o = sin(v[e.y]); break;
+      case OP_COS: o = cos(v[e.y]); break;
+      case OP_LOG: o = log(v[e.y]); break;
+      case OP_SQRT: o = sqrt(v[e.y]); break;
+      default: o = exp(v[e.y]); break;
+    }
+    v[i] = o;
+  }
+  double *out = contrib + B.contrib_off;
+  if (need_val) out[r] = v[B.out];
+  if (!need_first && !need_hess) return;
+
+  // ---- reverse sweep (expressions.py:287-314)
+  double adj[kMaxTape];
+  uint64_t amask = 1ull << B.out;
+  adj[B.out] = 1.0;
+  double g[kMaxSlots];
+  uint32_t gmask = 0;
+  for (int i = T - 1; i >= 0; --i) {
+    if (!((amask >> i) & 1ull)) continue;
+    int4 e = s_tape[i];
+    double ai = adj[i];
+    if (e.x == OP_VAR) {
+      if ((gmask >> e.y) & 1u) g[e.y] += ai; else { g[e.y] = ai; gmask |= 1u << e.y; }
+      continue;
+    }
+    if (e.x == OP_PAR || e.x == OP_CONST) continue;
+    Partials p = partials(e.x, e.y, e.z, i, v, s_const);
+    acc(adj, amask, e.y, p.fa * ai);
+    if (p.has_b) acc(adj, amask, e.z, p.fb * ai);
+  }
+  if (need_first)
+    for (int k = 0; k < B.nfirst; ++k) {
+      int s = first[k];
+      out[(1 + k) * R + r] = ((gmask >> s) & 1u) ? g[s] : 0.0;
+    }
+  if (!need_hess) return;
+
+  // ---- Hessian columns (expressions.py:316-409)
+  double w;
+  if (obj) w = obj_w;
+  else {
+    int t = targets[B.tgt_off + r];
+    w = y[t] * (con_scale ? con_scale[t] : 1.0);
+  }
+  const int64_t hbase = (1 + B.nfirst) * R;
+  for (int sw = 0; sw < B.nsweep; ++sw) {
+    const int ts = sweep[sw];
+    double dot[kMaxTape];
+    uint64_t dmask = 0;
+    for (int i = 0; i < T; ++i) {
+      int4 e = s_tape[i];
+      if (e.x == OP_VAR) {
+        if (e.y == ts) { dot[i] = 1.0; dmask |= 1ull << i; }
+        continue;
+      }
+      if (e.x == OP_PAR || e.x == OP_CONST) continue;
+      bool ha = (dmask >> e.y) & 1ull;
+      bool hb = is_binary(e.x) && ((dmask >> e.z) & 1ull);
+      if (!ha && !hb) continue;
+      Partials p = partials(e.x, e.y, e.z, i, v, s_const);
+      double t = 0.0;
+      bool have = false;
+      if (ha) { t = p.fa * dot[e.y]; have = true; }
+      if (hb) { t = have ? t + p.fb * dot[e.z] : p.fb * dot[e.z]; }
+      dot[i] = t;
+      dmask |= 1ull << i;
+    }
+    double adot[kMaxTape];
+    uint64_t admask = 0;
+    double hcol[kMaxSlots];
+    uint32_t hmask = 0;
+    for (int i = T - 1; i >= 0; --i) {
+      bool hai = (amask >> i) & 1ull;
+      bool hadi = (admask >> i) & 1ull;
+      if (!hai && !hadi) continue;
+      int4 e = s_tape[i];
+      if (e.x == OP_VAR) {
+        if (hadi) {
+          if ((hmask >> e.y) & 1u) hcol[e.y] += adot[i]; else { hcol[e.y] = adot[i]; hmask |= 1u << e.y; }
+        }
+        continue;
+      }
+      if (e.x == OP_PAR || e.x == OP_CONST) continue;
+      const int a = e.y, b = e.z;
+      Partials p = partials(e.x, a, b, i, v, s_const);
+      const bool hda = (dmask >> a) & 1ull;
+      const bool hdb = is_binary(e.x) && ((dmask >> b) & 1ull);
+      const double da = hda ? dot[a] : 0.0;
+      const double db = hdb ? dot[b] : 0.0;
+      double dfa = 0.0, dfb = 0.0;
+      bool hdfa = false, hdfb = false;
+      switch (e.x) {
+        case OP_MUL:
+          if (hdb) { dfa = db; hdfa = true; }
+          if (hda) { dfb = da; hdfb = true; }
+          break;
+        case OP_DIV: {
+          double vb = v[b];
+          if (hdb) { dfa = -db / (vb * vb); hdfa = true; }
+          if (hda) { dfb = -da / (vb * vb); hdfb = true; }
+          if (hdb) {
+            double t2 = 2.0 * v[a] * db / (vb * vb * vb);
+            dfb = hdfb ? dfb + t2 : t2;
+            hdfb = true;
+          }
+          break;
+        }
+        case OP_POW: {
+          double c = s_const[b];
+          if (hda && c != 1.0) { dfa = c * (c - 1.0) * powc(v[a], c - 2.0) * da; hdfa = true; }
+          break;
+        }
+        case OP_SIN: if (hda) { dfa = -sin(v[a]) * da; hdfa = true; } break;
+        case OP_COS: if (hda) { dfa = -cos(v[a]) * da; hdfa = true; } break;
+        case OP_LOG: if (hda) { dfa = -da / (v[a] * v[a]); hdfa = true; } break;
+        case OP_SQRT: if (hda) { dfa = -0.25 * da / (v[a] * v[i]); hdfa = true; } break;
+        case OP_EXP: if (hda) { dfa = v[i] * da; hdfa = true; } break;
+        default: break;  // ADD, SUB, NEG: constant partials
+      }
+      if (hai && hdfa) acc(adot, admask, a, dfa * adj[i]);
+      if (hadi) acc(adot, admask, a, p.fa * adot[i]);
+      if (p.has_b) {
+        if (hai && hdfb) acc(adot, admask, b, dfb * adj[i]);
+        if (hadi) acc(adot, admask, b, p.fb * adot[i]);
+      }
+    }
+    for (int k = 0; k < B.npairs; ++k) {
+      if (pair_b[k] != ts) continue;
+      const int a = pair_a[k];
+      double c = 0.0;
+      if (((hmask >> a) & 1u) && !(obj && obj_w == 0.0)) {
+        double fac = 1.0;
+        if (a != ts && var_idx[B.var_off + a * R + r] == var_idx[B.var_off + ts * R + r]) fac = 2.0;
+        c = (w * fac) * hcol[a];
+      }
+      out[hbase + k * R + r] = c;
+    }
+  }
+}
+
+struct GatherSeg {
+  int64_t n_out;
+  const int64_t *ptr;
+  const int32_t *src;
+  double *out;
+  int mode;  // 0 none, 1 scalar, 2 scale[o], 3 scale[rows[o]]
+  double scalar;
+  const double *scale;
+  const int32_t *rows;
+  int32_t bit;
+};
+
+struct GatherArgs {
+  GatherSeg seg[4];
+  int nseg;
+  int64_t begin[5];
+};
+
+__global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contrib, int32_t *flags) {
+  int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= ga.begin[ga.nseg]) return;
+  int s = 0;
+  while (t >= ga.begin[s + 1]) ++s;
+  const GatherSeg &G = ga.seg[s];
+  int64_t o = t - ga.begin[s];
+  double acc = 0.0;
+  for (int64_t p = G.ptr[o]; p < G.ptr[o + 1]; ++p) acc = __dadd_rn(acc, contrib[G.src[p]]);
+  if (!isfinite(acc)) atomicOr(flags, G.bit);
+  double sc = 1.0;
+  if (G.mode == 1) sc = G.scalar;
+  else if (G.mode == 2 && G.scale) sc = G.scale[o];
+  else if (G.mode == 3 && G.scale) sc = G.scale[G.rows[o]];
+  G.out[o] = G.mode == 0 ? acc : acc * sc;
+}
+
+// Objective: per-block fixed-order tree sums, blocks added in order.
+__global__ void ad_objective_kernel(const int32_t *__restrict__ src, const int64_t *__restrict__ bptr,
+                                    int nblk, const double *__restrict__ contrib, double scale,
+                                    double *f, int32_t *flags) {
+  __shared__ double red[256];
+  double total = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    double part = 0.0;
+    for (int64_t p = bptr[b] + threadIdx.x; p < bptr[b + 1]; p += blockDim.x) part += contrib[src[p]];
+    red[threadIdx.x] = part;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+      __syncthreads();
+    }
+    total += red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (!isfinite(total)) atomicOr(flags, GN_AD_F);
+    *f = total * scale;
+  }
+}
+
+}  // namespace
+
+Model::~Model() {
+  if (!uploaded) return;
+  void *ps[] = {d.blocks, d.tape, d.consts, d.slots, d.var_idx, d.params, d.targets, d.c_ptr,
+                d.grad_ptr, d.jac_ptr, d.hess_ptr, d.c_src, d.grad_src, d.jac_src, d.hess_src,
+                d.obj_src, d.jac_rows, d.obj_block_ptr};
+  for (void *p : ps) dev_free(p);
+}
+
+static void upload_model(Model &M) {
+  std::vector<DevBlock> db;
+  std::vector<int4> tape;
+  std::vector<double> consts;
+  std::vector<int32_t> slots, vidx, tg;
+  std::vector<double> par;
+  int64_t cta = 0, coff = 0;
+  for (auto &b : M.blocks) {
+    DevBlock d{};
+    d.kind = b.kind;
+    d.nv = b.nv;
+    d.np = b.np;
+    d.T = static_cast<int32_t>(b.ops.size() / 3);
+    d.out = b.out;
+    d.nfirst = static_cast<int32_t>(b.first.size());
+    d.npairs = static_cast<int32_t>(b.pairs.size() / 2);
+    d.R = b.R;
+    d.var_off = static_cast<int64_t>(vidx.size());
+    d.par_off = static_cast<int64_t>(par.size());
+    d.tgt_off = static_cast<int64_t>(tg.size());
+    d.contrib_off = coff;
+    coff += b.R * (1 + d.nfirst + d.npairs);
+    d.tape_off = static_cast<int32_t>(tape.size());
+    d.const_off = static_cast<int32_t>(consts.size());
+    d.nconst = static_cast<int32_t>(b.consts.size());
+    d.slot_off = static_cast<int32_t>(slots.size());
+    d.cta_begin = cta;
+    cta += (b.R + kRecThreads - 1) / kRecThreads;
+    for (int t = 0; t < d.T; ++t) tape.push_back(make_int4(b.ops[3 * t], b.ops[3 * t + 1], b.ops[3 * t + 2], 0));
+    consts.insert(consts.end(), b.consts.begin(), b.consts.end());
+    GN_REQUIRE(b.consts.size() <= static_cast<size_t>(kMaxTape), "too many constants in a tape");
+    for (int s : b.first) slots.push_back(s);
+    std::vector<int> sw;
+    for (int p = 0; p < d.npairs; ++p) slots.push_back(b.pairs[2 * p]);
+    for (int p = 0; p < d.npairs; ++p) {
+      slots.push_back(b.pairs[2 * p + 1]);
+      if (std::find(sw.begin(), sw.end(), b.pairs[2 * p + 1]) == sw.end()) sw.push_back(b.pairs[2 * p + 1]);
+    }
+    std::sort(sw.begin(), sw.end());
+    d.nsweep = static_cast<int32_t>(sw.size());
+    for (int s : sw) slots.push_back(s);
+    for (int s = 0; s < b.nv; ++s)
+      for (int64_t r = 0; r < b.R; ++r) vidx.push_back(static_cast<int32_t>(b.var_idx[r * b.nv + s]));
+    for (int s = 0; s < b.np; ++s)
+      for (int64_t r = 0; r < b.R; ++r) par.push_back(b.params[r * b.np + s]);
+    for (int64_t r = 0; r < static_cast<int64_t>(b.targets.size()); ++r) tg.push_back(static_cast<int32_t>(b.targets[r]));
+    db.push_back(d);
+  }
+  GN_REQUIRE(coff == M.n_contrib, "contribution layout mismatch");
+  GN_REQUIRE(coff < (int64_t(1) << 31), "contribution array too large for int32 gather lists");
+  M.dblocks = db;
+  M.n_ctas_rec = cta;
+  M.d.blocks = dev_upload(db);
+  M.d.tape = reinterpret_cast<int32_t *>(dev_upload(tape));
+  M.d.consts = dev_upload(consts);
+  M.d.slots = dev_upload(slots);
+  M.d.var_idx = dev_upload(vidx);
+  M.d.params = dev_upload(par);
+  M.d.targets = dev_upload(tg);
+  M.d.c_ptr = dev_upload(M.c_ptr);
+  M.d.grad_ptr = dev_upload(M.grad_ptr);
+  M.d.jac_ptr = dev_upload(M.jac_ptr);
+  M.d.hess_ptr = dev_upload(M.hess_ptr);
+  M.d.c_src = dev_upload(narrow<int32_t>(M.c_src));
+  M.d.grad_src = dev_upload(narrow<int32_t>(M.grad_src));
+  M.d.jac_src = dev_upload(narrow<int32_t>(M.jac_src));
+  M.d.hess_src = dev_upload(narrow<int32_t>(M.hess_src));
+  M.d.obj_src = dev_upload(narrow<int32_t>(M.obj_src));
+  M.d.obj_block_ptr = dev_upload(M.obj_block_ptr);
+  M.d.n_obj_blocks = static_cast<int32_t>(M.obj_block_ptr.size()) - 1;
+  M.d.jac_rows = dev_upload(narrow<int32_t>(M.jac_rows));
+  M.uploaded = true;
+}
+
+static void ad_eval(Model &M, const double *x, const double *y, double obj_w, const double *con_scale,
+                    double obj_scale, double *f, double *c, double *grad, double *jac, double *hess,
+                    uint32_t what, double *contrib, int32_t *flags, cudaStream_t st) {
+  GN_REQUIRE(M.uploaded, "model not uploaded to the device");
+  if (what & GN_AD_HESS) GN_REQUIRE(y != nullptr || M.m == 0, "Hessian needs multipliers");
+  if (M.n_ctas_rec > 0)
+    ad_records_kernel<<<static_cast<unsigned>(M.n_ctas_rec), kRecThreads, 0, st>>>(
+        M.d.blocks, static_cast<int>(M.dblocks.size()), reinterpret_cast<const int4 *>(M.d.tape),
+        M.d.consts, M.d.slots, M.d.var_idx, M.d.params, M.d.targets, x, y, con_scale, obj_w, what,
+        contrib);
+  GN_LAUNCH_CHECK();
+  GatherArgs ga{};
+  int ns = 0;
+  auto add = [&](int64_t n_out, const int64_t *ptr, const int32_t *src, double *out, int mode,
+                 double scalar, const double *scale, const int32_t *rows, int bit) {
+    if (n_out == 0) return;
+    ga.seg[ns] = GatherSeg{n_out, ptr, src, out, mode, scalar, scale, rows, bit};
+    ga.begin[ns + 1] = ga.begin[ns] + n_out;
+    ++ns;
+  };
+  ga.begin[0] = 0;
+  if (what & GN_AD_C) add(M.m, M.d.c_ptr, M.d.c_src, c, con_scale ? 2 : 0, 1.0, con_scale, nullptr, GN_AD_C);
+  if (what & GN_AD_GRAD) add(M.n, M.d.grad_ptr, M.d.grad_src, grad, obj_scale != 1.0 ? 1 : 0, obj_scale, nullptr, nullptr, GN_AD_GRAD);
+  if (what & GN_AD_JAC)
+    add(static_cast<int64_t>(M.jac_rows.size()), M.d.jac_ptr, M.d.jac_src, jac, con_scale ? 3 : 0, 1.0,
+        con_scale, M.d.jac_rows, GN_AD_JAC);
+  if (what & GN_AD_HESS)
+    add(static_cast<int64_t>(M.hess_rows.size()), M.d.hess_ptr, M.d.hess_src, hess, 0, 1.0, nullptr, nullptr, GN_AD_HESS);
+  ga.nseg = ns;
+  if (ns > 0) {
+    int64_t tot = ga.begin[ns];
+    ad_gather_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(ga, contrib, flags);
+    GN_LAUNCH_CHECK();
+  }
+  if (what & GN_AD_F) {
+    if (M.d.n_obj_blocks > 0) {
+      ad_objective_kernel<<<1, 256, 0, st>>>(M.d.obj_src, M.d.obj_block_ptr, M.d.n_obj_blocks, contrib,
+                                             obj_scale, f, flags);
+      GN_LAUNCH_CHECK();
+    } else {
+      GN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), st));
+    }
+  }
+}
+
+}  // namespace gn
+
+using namespace gn;
+
+extern "C" int gn_model_upload(gn_model *M) {
+  return guarded([&] {
+    if (!M->uploaded) upload_model(*M);
+  });
+}
+
+extern "C" int gn_ad_eval(gn_model *M, const double *x, const double *y, double obj_weight,
+                          const double *con_scale, double obj_scale, double *f, double *c,
+                          double *grad, double *jac, double *hess, uint32_t what, double *contrib_ws,
+                          int32_t *flags, void *stream) {
+  return guarded([&] {
+    ad_eval(*M, x, y, obj_weight, con_scale, obj_scale, f, c, grad, jac, hess, what, contrib_ws, flags,
+            static_cast<cudaStream_t>(stream));
+  });
+}

@@ -1,0 +1,66 @@
+// Device-side helpers shared by the CUDA translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace gn {
+
+#define GN_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      throw ::gn::Error(std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define GN_LAUNCH_CHECK() GN_CUDA(cudaGetLastError())
+
+template <class T>
+T *dev_upload(const std::vector<T> &v) {
+  T *p = nullptr;
+  size_t bytes = sizeof(T) * (v.empty() ? 1 : v.size());
+  GN_CUDA(cudaMalloc(&p, bytes));
+  if (!v.empty()) GN_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return p;
+}
+
+template <class T>
+T *dev_alloc(size_t count) {
+  T *p = nullptr;
+  GN_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+  return p;
+}
+
+template <class D, class S>
+std::vector<D> narrow(const std::vector<S> &v) {
+  std::vector<D> out(v.size());
+  for (size_t i = 0; i < v.size(); ++i) out[i] = static_cast<D>(v[i]);
+  return out;
+}
+
+inline void dev_free(void *p) {
+  if (p) cudaFree(p);
+}
+
+inline int sm_count() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 1;
+}
+
+// L2-coherent load for data produced by another CTA of the same launch.
+template <class T>
+__device__ __forceinline__ T ld_cg(const T *p) {
+  return __ldcg(p);
+}
+
+__device__ __forceinline__ int ld_volatile(const int *p) {
+  return *reinterpret_cast<const volatile int *>(p);
+}
+
+}  // namespace gn

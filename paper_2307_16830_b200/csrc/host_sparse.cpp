@@ -1,0 +1,493 @@
+// Host symbolic sparse linear algebra: condensation pattern, exact minimum
+// degree ordering, symbolic Cholesky and the supernodal (multifrontal) front
+// plan consumed by the CUDA factorisation in chol.cu.
+//
+// Reference semantics followed (bit-exact outputs):
+//   coo_to_csc          csc.py:52-76        (col<<32|row keys, np.unique inverse)
+//   symbolic_condense   kkt.py:243-283      (W, I, tril(A^T A) per Jacobian row)
+//   amd_order           amd.py:18-54        (greedy MD, key (deg, deg0, index))
+//   symbolic_cholesky   cholesky.py:94-144  (permute, etree 56-70, row
+//                                            patterns 73-91, L CSC)
+#include <cstring>
+#include <queue>
+#include <tuple>
+
+#include "internal.h"
+
+namespace gn {
+
+// keys (col << 32 | row) -> sorted unique + inverse map
+static void csc_from_keys(int64_t n, const std::vector<uint64_t> &keys, std::vector<int64_t> &indptr,
+                          std::vector<int64_t> &indices, std::vector<int64_t> &slot) {
+  std::vector<uint64_t> u(keys);
+  sort_unique(u);
+  indptr.assign(n + 1, 0);
+  indices.resize(u.size());
+  for (size_t i = 0; i < u.size(); ++i) {
+    int64_t c = static_cast<int64_t>(u[i] >> 32);
+    GN_REQUIRE(c >= 0 && c < n, "column out of range");
+    indptr[c + 1]++;
+    indices[i] = static_cast<int64_t>(u[i] & 0xFFFFFFFFull);
+  }
+  for (int64_t j = 0; j < n; ++j) indptr[j + 1] += indptr[j];
+  slot.resize(keys.size());
+  for (size_t t = 0; t < keys.size(); ++t)
+    slot[t] = std::lower_bound(u.begin(), u.end(), keys[t]) - u.begin();
+}
+
+static inline uint64_t ckey(int64_t row, int64_t col) {
+  return (static_cast<uint64_t>(col) << 32) | static_cast<uint64_t>(row);
+}
+
+static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc,
+                     int64_t nj, const int64_t *jr, const int64_t *jc) {
+  C.n = n;
+  C.nnz_h = nh;
+  C.nnz_j = nj;
+  for (int64_t t = 1; t < nj; ++t)
+    GN_REQUIRE(jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1]),
+               "Jacobian coordinates must be sorted row-major and unique");
+  std::vector<uint64_t> keys;
+  keys.reserve(nh + n);
+  for (int64_t t = 0; t < nh; ++t) {
+    GN_REQUIRE(hc[t] <= hr[t], "Hessian entry above the diagonal");
+    keys.push_back(ckey(hr[t], hc[t]));
+  }
+  for (int64_t i = 0; i < n; ++i) keys.push_back(ckey(i, i));
+  C.ata_row.clear();
+  C.ata_s1.clear();
+  C.ata_s2.clear();
+  int64_t st = 0;
+  while (st < nj) {
+    int64_t en = st;
+    while (en < nj && jr[en] == jr[st]) ++en;
+    // np.tril_indices(k): row-major over the lower triangle
+    for (int64_t la = 0; la < en - st; ++la)
+      for (int64_t lb = 0; lb <= la; ++lb) {
+        keys.push_back(ckey(jc[st + la], jc[st + lb]));
+        C.ata_row.push_back(jr[st]);
+        C.ata_s1.push_back(st + la);
+        C.ata_s2.push_back(st + lb);
+      }
+    st = en;
+  }
+  std::vector<int64_t> slot;
+  csc_from_keys(n, keys, C.indptr, C.indices, slot);
+  C.w_map.assign(slot.begin(), slot.begin() + nh);
+  C.diag_map.assign(slot.begin() + nh, slot.begin() + nh + n);
+  C.ata_map.assign(slot.begin() + nh + n, slot.end());
+}
+
+// ------------------------------------------------------------ ordering
+static void min_degree(int64_t n, const int64_t *indptr, const int64_t *indices, int64_t *perm) {
+  std::vector<std::vector<int32_t>> adj(n);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
+      int64_t i = indices[p];
+      if (i != j) {
+        adj[i].push_back(static_cast<int32_t>(j));
+        adj[j].push_back(static_cast<int32_t>(i));
+      }
+    }
+  for (auto &a : adj) {
+    std::sort(a.begin(), a.end());
+    a.erase(std::unique(a.begin(), a.end()), a.end());
+  }
+  std::vector<int64_t> deg(n), deg0(n);
+  std::vector<char> alive(n, 1);
+  using Key = std::tuple<int64_t, int64_t, int64_t>;
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
+  for (int64_t v = 0; v < n; ++v) {
+    deg[v] = deg0[v] = static_cast<int64_t>(adj[v].size());
+    heap.emplace(deg[v], deg0[v], v);
+  }
+  std::vector<int32_t> merged;
+  for (int64_t k = 0; k < n; ++k) {
+    int64_t v;
+    for (;;) {
+      auto [d, d0, u] = heap.top();
+      heap.pop();
+      if (alive[u] && d == deg[u]) {
+        v = u;
+        break;
+      }
+    }
+    perm[k] = v;
+    alive[v] = 0;
+    std::vector<int32_t> nb;
+    nb.swap(adj[v]);
+    // clique formation (amd.py:49-53): adj[u] = adj[u] | nb  minus {u, v}
+    for (int32_t u : nb) {
+      auto &au = adj[u];
+      merged.clear();
+      merged.reserve(au.size() + nb.size());
+      size_t a = 0, b = 0;
+      while (a < au.size() || b < nb.size()) {
+        int32_t x;
+        if (b == nb.size() || (a < au.size() && au[a] < nb[b])) {
+          x = au[a++];
+        } else if (a == au.size() || nb[b] < au[a]) {
+          x = nb[b++];
+        } else {
+          x = au[a++];
+          ++b;
+        }
+        if (x != u && x != v) merged.push_back(x);
+      }
+      au.swap(merged);
+    }
+    for (int32_t u : nb) {
+      int64_t nd = static_cast<int64_t>(adj[u].size());
+      if (nd != deg[u]) {
+        deg[u] = nd;
+        heap.emplace(nd, deg0[u], u);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------ symbolic Cholesky
+static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_t *indices,
+                     const int64_t *perm) {
+  S.n = n;
+  int64_t nnz = indptr[n];
+  S.nnz_a = nnz;
+  S.perm.assign(perm, perm + n);
+  std::vector<int64_t> pinv(n, -1);
+  for (int64_t k = 0; k < n; ++k) {
+    GN_REQUIRE(perm[k] >= 0 && perm[k] < n && pinv[perm[k]] == -1, "ordering is not a permutation");
+    pinv[perm[k]] = k;
+  }
+  std::vector<int64_t> prow(nnz), pcol(nnz);
+  for (int64_t j = 0; j < n; ++j)
+    for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
+      int64_t a = pinv[indices[p]], b = pinv[j];
+      prow[p] = std::max(a, b);
+      pcol[p] = std::min(a, b);
+    }
+  // stable sort by (prow, pcol): counting sort on pcol, then on prow
+  std::vector<int64_t> cnt(n + 1), o1(nnz), o2(nnz);
+  for (int64_t p = 0; p < nnz; ++p) cnt[pcol[p] + 1]++;
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  for (int64_t p = 0; p < nnz; ++p) o1[cnt[pcol[p]]++] = p;
+  std::fill(cnt.begin(), cnt.end(), 0);
+  for (int64_t p = 0; p < nnz; ++p) cnt[prow[p] + 1]++;
+  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
+  S.a_rowptr.assign(cnt.begin(), cnt.end());
+  for (int64_t t = 0; t < nnz; ++t) {
+    int64_t p = o1[t];
+    o2[cnt[prow[p]]++] = p;
+  }
+  S.a_rowcol.resize(nnz);
+  S.a_srcslot = o2;
+  for (int64_t t = 0; t < nnz; ++t) S.a_rowcol[t] = pcol[o2[t]];
+  // elimination tree (cholesky.py:56-70)
+  S.parent.assign(n, -1);
+  std::vector<int64_t> anc(n, -1);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
+      int64_t i = S.a_rowcol[t];
+      while (anc[i] != -1 && anc[i] != k) {
+        int64_t nx = anc[i];
+        anc[i] = k;
+        i = nx;
+      }
+      if (anc[i] == -1 && i != k) {
+        anc[i] = k;
+        S.parent[i] = k;
+      }
+    }
+  // row patterns (cholesky.py:73-91)
+  std::vector<int64_t> mark(n, -1);
+  S.row_ptr.assign(n + 1, 0);
+  S.row_cols.clear();
+  std::vector<int64_t> pat;
+  for (int64_t k = 0; k < n; ++k) {
+    pat.clear();
+    mark[k] = k;
+    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
+      int64_t i = S.a_rowcol[t];
+      while (i != -1 && mark[i] != k) {
+        mark[i] = k;
+        pat.push_back(i);
+        i = S.parent[i];
+      }
+    }
+    std::sort(pat.begin(), pat.end());
+    S.row_cols.insert(S.row_cols.end(), pat.begin(), pat.end());
+    S.row_ptr[k + 1] = static_cast<int64_t>(S.row_cols.size());
+  }
+  // L in CSC, diagonal first, rows increasing (cholesky.py:118-131)
+  std::vector<int64_t> counts(n, 1);
+  for (int64_t j : S.row_cols) counts[j]++;
+  S.l_colptr.assign(n + 1, 0);
+  for (int64_t j = 0; j < n; ++j) S.l_colptr[j + 1] = S.l_colptr[j] + counts[j];
+  S.l_rowidx.assign(S.l_colptr[n], 0);
+  std::vector<int64_t> fill(S.l_colptr.begin(), S.l_colptr.end() - 1);
+  for (int64_t j = 0; j < n; ++j) S.l_rowidx[fill[j]++] = j;
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) S.l_rowidx[fill[S.row_cols[t]]++] = k;
+}
+
+// ------------------------------------------------------------ front plan
+// Supernodes are maximal runs j, j+1, ... with parent[j] == j+1 (contiguous in
+// the reference elimination order, so the reference's pivot sequence is kept),
+// relaxed: a column joins the running supernode when the explicit zeros stay
+// below a width-dependent fraction (CHOLMOD-style amalgamation rule).
+static void front_plan(Symbolic &S) {
+  const int64_t n = S.n;
+  std::vector<int64_t> cc(n);
+  for (int64_t j = 0; j < n; ++j) cc[j] = S.l_colptr[j + 1] - S.l_colptr[j];
+  std::vector<int32_t> snode_of(n);
+  S.f_first.clear();
+  S.f_ncols.clear();
+  int64_t f = 0;
+  int64_t true_nnz = cc[0];
+  for (int64_t j = 1; j <= n; ++j) {
+    bool join = false;
+    if (j < n && S.parent[j - 1] == j) {
+      int64_t w = j - f + 1;               // width if column j joins
+      int64_t s = w + cc[j] - 1;           // front rows: [f..j] + struct(j)
+      int64_t dense = w * s - w * (w - 1) / 2;
+      int64_t tn = true_nnz + cc[j];
+      double zfrac = static_cast<double>(dense - tn) / static_cast<double>(dense);
+      if (cc[j - 1] == cc[j] + 1) join = true;  // fundamental: no new zeros
+      else if (w <= 4) join = true;
+      else if (w <= 16 && zfrac < 0.5) join = true;
+      else if (w <= 48 && zfrac < 0.1) join = true;
+      else if (zfrac < 0.05) join = true;
+    }
+    if (join) {
+      true_nnz += cc[j];
+      continue;
+    }
+    S.f_first.push_back(static_cast<int32_t>(f));
+    S.f_ncols.push_back(static_cast<int32_t>(j - f));
+    if (j < n) {
+      f = j;
+      true_nnz = cc[j];
+    }
+  }
+  const int64_t nf = static_cast<int64_t>(S.f_first.size());
+  S.nf = nf;
+  for (int64_t J = 0; J < nf; ++J)
+    for (int64_t c = S.f_first[J]; c < S.f_first[J] + S.f_ncols[J]; ++c) snode_of[c] = static_cast<int32_t>(J);
+  // rows, sizes, offsets
+  S.f_nrows.resize(nf);
+  S.f_parent.assign(nf, -1);
+  S.f_rows_off.assign(nf + 1, 0);
+  S.f_rows.clear();
+  S.f_off.assign(nf + 1, 0);
+  S.f_voff.assign(nf + 1, 0);
+  S.max_front = S.max_cols = 0;
+  S.flops = 0;
+  for (int64_t J = 0; J < nf; ++J) {
+    int64_t first = S.f_first[J], w = S.f_ncols[J], l = first + w - 1;
+    for (int64_t c = first; c <= l; ++c) S.f_rows.push_back(static_cast<int32_t>(c));
+    for (int64_t p = S.l_colptr[l] + 1; p < S.l_colptr[l + 1]; ++p)
+      S.f_rows.push_back(static_cast<int32_t>(S.l_rowidx[p]));
+    int64_t s = w + cc[l] - 1;
+    S.f_nrows[J] = static_cast<int32_t>(s);
+    S.f_rows_off[J + 1] = static_cast<int64_t>(S.f_rows.size());
+    S.f_off[J + 1] = S.f_off[J] + s * s;
+    S.f_voff[J + 1] = S.f_voff[J] + s;
+    S.max_front = std::max(S.max_front, s);
+    S.max_cols = std::max(S.max_cols, w);
+    if (S.parent[l] != -1) S.f_parent[J] = snode_of[S.parent[l]];
+    for (int64_t c = 0; c < w; ++c) S.flops += (s - c - 1) * (s - c - 1) + 2 * (s - c);
+  }
+  S.front_doubles = S.f_off[nf];
+  S.vec_doubles = S.f_voff[nf];
+  // children CSR (increasing child index)
+  S.f_child_ptr.assign(nf + 1, 0);
+  for (int64_t J = 0; J < nf; ++J)
+    if (S.f_parent[J] >= 0) S.f_child_ptr[S.f_parent[J] + 1]++;
+  for (int64_t J = 0; J < nf; ++J) S.f_child_ptr[J + 1] += S.f_child_ptr[J];
+  S.f_child.assign(S.f_child_ptr[nf], 0);
+  {
+    std::vector<int32_t> fl(S.f_child_ptr.begin(), S.f_child_ptr.end() - 1);
+    for (int64_t J = 0; J < nf; ++J)
+      if (S.f_parent[J] >= 0) S.f_child[fl[S.f_parent[J]]++] = static_cast<int32_t>(J);
+  }
+  auto local = [&](int64_t J, int64_t row) -> int64_t {
+    const int32_t *b = S.f_rows.data() + S.f_rows_off[J];
+    const int32_t *e = S.f_rows.data() + S.f_rows_off[J + 1];
+    const int32_t *it = std::lower_bound(b, e, static_cast<int32_t>(row));
+    GN_REQUIRE(it != e && *it == row, "row missing from front structure");
+    return it - b;
+  };
+  // relmaps: child update rows (rows past its pivot block) in the parent front
+  S.f_relmap_off.assign(nf + 1, 0);
+  S.relmap.clear();
+  for (int64_t C = 0; C < nf; ++C) {
+    int64_t w = S.f_ncols[C], s = S.f_nrows[C], P = S.f_parent[C];
+    if (P >= 0)
+      for (int64_t i = w; i < s; ++i)
+        S.relmap.push_back(static_cast<int32_t>(local(P, S.f_rows[S.f_rows_off[C] + i])));
+    else
+      GN_REQUIRE(s == w, "root front with an update block");
+    S.f_relmap_off[C + 1] = static_cast<int64_t>(S.relmap.size());
+  }
+  // A scatter (permuted lower entries, grouped by front)
+  std::vector<int64_t> per(nf + 1, 0);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) per[snode_of[S.a_rowcol[t]] + 1]++;
+  for (int64_t J = 0; J < nf; ++J) per[J + 1] += per[J];
+  S.f_a_ptr = per;
+  S.a_kslot.assign(per[nf], 0);
+  S.a_fpos.assign(per[nf], 0);
+  {
+    std::vector<int64_t> fl(per.begin(), per.end() - 1);
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
+        int64_t j = S.a_rowcol[t];
+        int64_t J = snode_of[j];
+        int64_t lr = local(J, k), lc = j - S.f_first[J];
+        int64_t q = fl[J]++;
+        S.a_kslot[q] = S.a_srcslot[t];
+        S.a_fpos[q] = S.f_off[J] + lc * S.f_nrows[J] + lr;
+      }
+  }
+  // reference L layout -> front storage
+  S.l_export.assign(S.l_rowidx.size(), 0);
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t J = snode_of[j], lc = j - S.f_first[J];
+    for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p)
+      S.l_export[p] = S.f_off[J] + lc * S.f_nrows[J] + local(J, S.l_rowidx[p]);
+  }
+  // levels (leaves 0) and task order
+  S.level.assign(nf, 0);
+  int64_t maxl = 0;
+  for (int64_t J = 0; J < nf; ++J) {  // children precede parents in index order
+    for (int32_t t = S.f_child_ptr[J]; t < S.f_child_ptr[J + 1]; ++t)
+      S.level[J] = std::max(S.level[J], S.level[S.f_child[t]] + 1);
+    maxl = std::max<int64_t>(maxl, S.level[J]);
+  }
+  S.n_levels = nf ? maxl + 1 : 0;
+  S.order.resize(nf);
+  {
+    std::vector<int64_t> lc(S.n_levels + 1, 0);
+    for (int64_t J = 0; J < nf; ++J) lc[S.level[J] + 1]++;
+    for (int64_t l = 0; l < S.n_levels; ++l) lc[l + 1] += lc[l];
+    for (int64_t J = 0; J < nf; ++J) S.order[lc[S.level[J]]++] = static_cast<int32_t>(J);
+  }
+}
+
+}  // namespace gn
+
+using namespace gn;
+
+extern "C" int gn_condense_create(int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc,
+                                  int64_t nj, const int64_t *jr, const int64_t *jc,
+                                  gn_condense **out) {
+  return guarded([&] {
+    auto *C = new gn_condense();
+    try {
+      condense(*C, n, nh, hr, hc, nj, jr, jc);
+    } catch (...) {
+      delete C;
+      throw;
+    }
+    *out = C;
+  });
+}
+
+extern "C" int gn_condense_info(const gn_condense *C, int64_t *nnz_k, int64_t *np) {
+  return guarded([&] {
+    if (nnz_k) *nnz_k = static_cast<int64_t>(C->indices.size());
+    if (np) *np = static_cast<int64_t>(C->ata_map.size());
+  });
+}
+
+template <class T>
+static void copy_out(T *dst, const std::vector<T> &v) {
+  if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(T) * v.size());
+}
+
+extern "C" int gn_condense_export(const gn_condense *C, int64_t *indptr, int64_t *indices,
+                                  int64_t *w_map, int64_t *diag_map, int64_t *ata_map,
+                                  int64_t *ata_row, int64_t *ata_s1, int64_t *ata_s2) {
+  return guarded([&] {
+    copy_out(indptr, C->indptr);
+    copy_out(indices, C->indices);
+    copy_out(w_map, C->w_map);
+    copy_out(diag_map, C->diag_map);
+    copy_out(ata_map, C->ata_map);
+    copy_out(ata_row, C->ata_row);
+    copy_out(ata_s1, C->ata_s1);
+    copy_out(ata_s2, C->ata_s2);
+  });
+}
+
+extern "C" void gn_condense_destroy(gn_condense *C) { delete C; }
+
+extern "C" int gn_coo_to_csc(int64_t n, int64_t nnz, const int64_t *rows, const int64_t *cols,
+                             int64_t *nnz_out, int64_t *indptr_out, int64_t *indices_out,
+                             int64_t *slot_out) {
+  return guarded([&] {
+    std::vector<uint64_t> keys(nnz);
+    for (int64_t t = 0; t < nnz; ++t) {
+      GN_REQUIRE(rows[t] >= 0 && rows[t] < n && cols[t] >= 0 && cols[t] < n, "index out of range");
+      GN_REQUIRE(cols[t] <= rows[t], "entry above the diagonal");
+      keys[t] = ckey(rows[t], cols[t]);
+    }
+    std::vector<int64_t> indptr, indices, slot;
+    csc_from_keys(n, keys, indptr, indices, slot);
+    if (nnz_out) *nnz_out = static_cast<int64_t>(indices.size());
+    copy_out(indptr_out, indptr);
+    copy_out(indices_out, indices);
+    copy_out(slot_out, slot);
+  });
+}
+
+extern "C" int gn_min_degree(int64_t n, const int64_t *indptr, const int64_t *indices, int64_t *perm) {
+  return guarded([&] { min_degree(n, indptr, indices, perm); });
+}
+
+extern "C" int gn_symbolic_create(int64_t n, const int64_t *indptr, const int64_t *indices,
+                                  const int64_t *perm, gn_symbolic **out) {
+  return guarded([&] {
+    GN_REQUIRE(n < (int64_t(1) << 31), "matrix too large for 32-bit device indices");
+    auto *S = new gn_symbolic();
+    try {
+      symbolic(*S, n, indptr, indices, perm);
+      if (n > 0) front_plan(*S);
+    } catch (...) {
+      delete S;
+      throw;
+    }
+    *out = S;
+  });
+}
+
+extern "C" int gn_symbolic_info(const gn_symbolic *S, gn_symbolic_info_t *info) {
+  return guarded([&] {
+    info->n = S->n;
+    info->nnz_a = S->nnz_a;
+    info->nnz_l = static_cast<int64_t>(S->l_rowidx.size());
+    info->n_fronts = S->nf;
+    info->front_doubles = S->front_doubles;
+    info->vec_doubles = S->vec_doubles;
+    info->max_front = S->max_front;
+    info->max_cols = S->max_cols;
+    info->n_levels = S->n_levels;
+    info->flops = S->flops;
+  });
+}
+
+extern "C" int gn_symbolic_export(const gn_symbolic *S, int64_t *parent, int64_t *a_rowptr,
+                                  int64_t *a_rowcol, int64_t *a_srcslot, int64_t *row_ptr,
+                                  int64_t *row_cols, int64_t *l_colptr, int64_t *l_rowidx) {
+  return guarded([&] {
+    copy_out(parent, S->parent);
+    copy_out(a_rowptr, S->a_rowptr);
+    copy_out(a_rowcol, S->a_rowcol);
+    copy_out(a_srcslot, S->a_srcslot);
+    copy_out(row_ptr, S->row_ptr);
+    copy_out(row_cols, S->row_cols);
+    copy_out(l_colptr, S->l_colptr);
+    copy_out(l_rowidx, S->l_rowidx);
+  });
+}
+
+extern "C" void gn_symbolic_destroy(gn_symbolic *S) { delete S; }

@@ -1,0 +1,178 @@
+// Internal definitions shared by the host symbolic code and the CUDA kernels.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/gridopf.h"
+
+namespace gn {
+
+// Sorted unique 64-bit keys (LSD radix sort for large inputs).
+inline void sort_unique(std::vector<uint64_t> &k) {
+  // LSD radix sort on 64-bit keys (8 passes of 8 bits would be slow for small
+  // inputs; use std::sort below 1M keys).
+  if (k.size() < (1u << 20)) {
+    std::sort(k.begin(), k.end());
+  } else {
+    std::vector<uint64_t> tmp(k.size());
+    for (int shift = 0; shift < 64; shift += 16) {
+      std::vector<size_t> cnt(65537, 0);
+      for (uint64_t v : k) cnt[((v >> shift) & 0xFFFF) + 1]++;
+      for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+      for (uint64_t v : k) tmp[cnt[(v >> shift) & 0xFFFF]++] = v;
+      k.swap(tmp);
+    }
+  }
+  k.erase(std::unique(k.begin(), k.end()), k.end());
+}
+
+
+void set_error(const std::string &msg);
+
+struct Error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define GN_REQUIRE(cond, msg)                         \
+  do {                                                \
+    if (!(cond)) throw ::gn::Error(std::string(msg)); \
+  } while (0)
+
+// Guard for extern "C" entry points: C++ exceptions never cross the ABI.
+template <class F>
+int guarded(F &&f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception &e) {
+    set_error(e.what());
+    return -1;
+  } catch (...) {
+    set_error("unknown error");
+    return -1;
+  }
+}
+
+constexpr int kMaxTape = 64;   // device interpreter: tape entries per instruction
+constexpr int kMaxSlots = 16;  // variable slots per record
+
+// ---------------------------------------------------------------- AD plan
+struct DevBlock {                // one pattern block as seen by the device
+  int32_t kind;                  // 0 obj, 1 define, 2 increment
+  int32_t nv, np, T, out;
+  int32_t nfirst, npairs, nsweep, nconst;
+  int64_t R;
+  int64_t var_off, par_off, tgt_off;   // into SoA record arrays
+  int64_t contrib_off;                 // [value | first slots | pairs] x R
+  int32_t tape_off, const_off;         // into the tape pools
+  int32_t slot_off;                    // into the small per-block int pool
+  int32_t spec;                        // specialised kernel id, 0 = interpreter
+  int64_t cta_begin;                   // first CTA of this block in the record launch
+};
+
+struct Model {
+  int64_t n = 0, m = 0;
+  // host copies of the blocks (canonical order)
+  struct HBlock {
+    int32_t kind, nv, np, out;
+    int64_t R;
+    std::vector<int64_t> var_idx;  // row-major R x nv
+    std::vector<double> params;    // row-major R x np
+    std::vector<int64_t> targets;
+    std::vector<int32_t> ops;      // T x 3
+    std::vector<double> consts;
+    std::vector<int32_t> first, pairs, grad_order;
+  };
+  std::vector<HBlock> blocks;
+  std::vector<int64_t> jac_rows, jac_cols, hess_rows, hess_cols;
+  std::vector<int64_t> jac_slots, hess_slots;  // concatenated (see gridopf.h)
+  std::vector<double> hess_factor;
+  int64_t n_contrib = 0;
+  // gather plans over contribution ids (CSR)
+  std::vector<int64_t> c_ptr, grad_ptr, jac_ptr, hess_ptr;
+  std::vector<int64_t> c_src, grad_src, jac_src, hess_src;
+  std::vector<int64_t> obj_src;  // objective value contributions, block order
+  std::vector<int64_t> obj_block_ptr;
+  // device
+  bool uploaded = false;
+  std::vector<DevBlock> dblocks;
+  int64_t n_ctas_rec = 0;
+  struct Dev {
+    DevBlock *blocks = nullptr;
+    int32_t *tape = nullptr;  // int4-packed (op, a, b, 0)
+    double *consts = nullptr;
+    int32_t *slots = nullptr;  // per block: first[], pair a/b[], sweep[], grad_order[]
+    int32_t *var_idx = nullptr;  // SoA int32
+    double *params = nullptr;    // SoA
+    int32_t *targets = nullptr;
+    int64_t *c_ptr = nullptr, *grad_ptr = nullptr, *jac_ptr = nullptr, *hess_ptr = nullptr;
+    int32_t *c_src = nullptr, *grad_src = nullptr, *jac_src = nullptr, *hess_src = nullptr;
+    int32_t *obj_src = nullptr;
+    int32_t *jac_rows = nullptr;
+    int64_t *obj_block_ptr = nullptr;
+    int32_t n_obj_blocks = 0;
+  } d;
+  ~Model();
+};
+
+// --------------------------------------------------------- condensation
+struct Condense {
+  int64_t n = 0, nnz_h = 0, nnz_j = 0;
+  std::vector<int64_t> indptr, indices;
+  std::vector<int64_t> w_map, diag_map, ata_map, ata_row, ata_s1, ata_s2;
+};
+
+// ------------------------------------------------------- symbolic factor
+struct Symbolic {
+  int64_t n = 0, nnz_a = 0;
+  std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, row_cols,
+      l_colptr, l_rowidx;
+  // ---- supernodal front plan (internal order = reference elimination order)
+  int64_t nf = 0;                              // number of fronts
+  std::vector<int32_t> f_first, f_ncols, f_nrows, f_parent;
+  std::vector<int64_t> f_rows_off;             // into f_rows
+  std::vector<int32_t> f_rows;                 // sorted internal row indices per front
+  std::vector<int64_t> f_off;                  // F storage offset (doubles)
+  std::vector<int64_t> f_voff;                 // solve scratch offset (doubles)
+  std::vector<int32_t> f_child_ptr, f_child;   // CSR children
+  std::vector<int64_t> f_relmap_off;           // per front: r entries into relmap
+  std::vector<int32_t> relmap;                 // child update rows -> parent local rows
+  std::vector<int64_t> f_a_ptr;                // CSR A scatter per front
+  std::vector<int64_t> a_kslot, a_fpos;        // (kvals slot, F offset)
+  std::vector<int32_t> order;                  // task order, leaves first
+  std::vector<int32_t> level;
+  std::vector<int64_t> l_export;               // reference L slot -> F offset
+  int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
+  int64_t flops = 0;
+  // device
+  bool uploaded = false;
+  struct Dev {
+    int32_t *f_first = nullptr, *f_ncols = nullptr, *f_nrows = nullptr, *f_parent = nullptr;
+    int64_t *f_rows_off = nullptr;
+    int32_t *f_rows = nullptr;
+    int64_t *f_off = nullptr, *f_voff = nullptr;
+    int32_t *f_child_ptr = nullptr, *f_child = nullptr;
+    int64_t *f_relmap_off = nullptr;
+    int32_t *relmap = nullptr;
+    int64_t *f_a_ptr = nullptr;
+    int32_t *a_kslot = nullptr;
+    int64_t *a_fpos = nullptr;
+    int32_t *order = nullptr;
+    int32_t *nchild = nullptr;        // template counters
+    int32_t *counters = nullptr;      // scratch counters
+    int32_t *task = nullptr;          // task queue heads
+    int64_t *l_export = nullptr;
+    int64_t *perm = nullptr;          // internal position -> original index
+  } d;
+  ~Symbolic();
+};
+
+}  // namespace gn
+
+struct gn_model : gn::Model {};
+struct gn_condense : gn::Condense {};
+struct gn_symbolic : gn::Symbolic {};

@@ -1,0 +1,543 @@
+// Condensed-KKT device kernels: matvecs, condensed assembly, right-hand
+// side, recoveries, the double-double seven-block residual and the matrix
+// scale (reference src/gridnlp/kkt.py:96-229, 300-312).
+//
+// Every kernel is a gather: each output entry is owned by one thread and
+// accumulates its inputs in the order the reference's np.add.at scatter
+// would, so values are deterministic and -- for the FMA-free assembly --
+// bitwise equal to the reference given equal inputs.
+#include <cmath>
+
+#include "reduce.cuh"
+
+namespace gn {
+
+struct Kkt {
+  int64_t n = 0, m = 0, nh = 0, nj = 0, nk = 0;
+  bool has_assembly = false;
+  struct Dev {
+    int64_t *a_rowptr = nullptr;   // A by rows (jac order)
+    int32_t *a_col = nullptr;
+    int64_t *at_ptr = nullptr;     // A by columns: jac positions + rows
+    int32_t *at_p = nullptr, *at_row = nullptr;
+    int64_t *w_ptr = nullptr;      // symmetric W per row: hess positions + partner
+    int32_t *w_p = nullptr, *w_j = nullptr;
+    int64_t *k_ptr = nullptr;      // assembly: per K slot products (row, s1, s2)
+    int32_t *k_row = nullptr, *k_s1 = nullptr, *k_s2 = nullptr;
+    int32_t *k_w = nullptr, *k_diag = nullptr;
+    double *partials = nullptr;
+    unsigned int *counter = nullptr;
+    double *scratch = nullptr;     // m doubles
+  } d;
+  ~Kkt() {
+    void *ps[] = {d.a_rowptr, d.a_col, d.at_ptr, d.at_p, d.at_row, d.w_ptr, d.w_p, d.w_j,
+                  d.k_ptr, d.k_row, d.k_s1, d.k_s2, d.k_w, d.k_diag, d.partials, d.counter,
+                  d.scratch};
+    for (void *p : ps) dev_free(p);
+  }
+};
+
+}  // namespace gn
+
+struct gn_kkt : gn::Kkt {};
+
+namespace gn {
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ double inv_or_zero(double w) { return isfinite(w) ? 1.0 / w : 0.0; }
+
+unsigned blocks_for(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT > 0 ? (n + kT - 1) / kT : 1); }
+
+// ------------------------------------------------------------ double-double
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd quick(double s, double e) {
+  double h = s + e;
+  return {h, e - (h - s)};
+}
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+  dd s = two_sum(x.hi, y.hi);
+  dd t = two_sum(x.lo, y.lo);
+  double e = s.lo + t.hi;
+  dd u = quick(s.hi, e);
+  return quick(u.hi, t.lo + u.lo);
+}
+__device__ __forceinline__ dd dd_prod(double a, double b) {
+  double p = a * b;
+  return {p, fma(a, b, -p)};
+}
+__device__ __forceinline__ dd dd_neg(dd x) { return {-x.hi, -x.lo}; }
+__device__ __forceinline__ dd dd_from(double a) { return {a, 0.0}; }
+// dd * double
+__device__ __forceinline__ dd dd_mul_d(dd x, double b) {
+  dd p = dd_prod(x.hi, b);
+  return quick(p.hi, p.lo + x.lo * b);
+}
+__device__ __forceinline__ double dd_round(dd x) { return x.hi + x.lo; }
+
+// ------------------------------------------------------------ kernels
+__global__ void sigma_kernel(int64_t len, const double *dl, const double *du, const double *zl,
+                             const double *zu, double *out) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i < len) out[i] = zl[i] * inv_or_zero(dl[i]) + zu[i] * inv_or_zero(du[i]);
+}
+
+// W v from the lower triangle: first every entry's row contribution, then
+// the mirrored off-diagonal contributions (kkt.py:132-138)
+__global__ void w_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *wp, const int32_t *wj,
+                                const double *w, const double *v, double *out) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int64_t t = ptr[i]; t < ptr[i + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(w[wp[t]], v[wj[t]]));
+  out[i] = acc;
+}
+
+__global__ void a_matvec_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, const double *a,
+                                const double *v, double *out) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i >= m) return;
+  double acc = 0.0;
+  for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) acc = __dadd_rn(acc, __dmul_rn(a[p], v[col[p]]));
+  out[i] = acc;
+}
+
+__global__ void at_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *pp, const int32_t *row,
+                                 const double *a, const double *u, double *out) {
+  int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (j >= n) return;
+  double acc = 0.0;
+  for (int64_t t = ptr[j]; t < ptr[j + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(a[pp[t]], u[row[t]]));
+  out[j] = acc;
+}
+
+// K[slot] = ((0 + W) + (sigma_x + dw)) + sum (d[row] * a[s1]) * a[s2] in
+// product order (kkt.py:300-312); no FMA contraction.
+__global__ void assemble_kernel(int64_t nk, const int64_t *kp, const int32_t *krow, const int32_t *ks1,
+                                const int32_t *ks2, const int32_t *kw, const int32_t *kd,
+                                gn_kkt_state st, double *K) {
+  int64_t s = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (s >= nk) return;
+  double acc = 0.0;
+  int w = kw[s];
+  if (w >= 0) acc = __dadd_rn(acc, st.w[w]);
+  int dg = kd[s];
+  if (dg >= 0) acc = __dadd_rn(acc, __dadd_rn(st.sx[dg], st.dw));
+  const double cfac = __dadd_rn(1.0, __dmul_rn(st.dc, st.dw));
+  for (int64_t p = kp[s]; p < kp[s + 1]; ++p) {
+    const int r = krow[p];
+    const double ssr = st.ss[r];
+    const double c = 1.0 / __dadd_rn(__dmul_rn(st.dc, ssr), cfac);
+    const double d = __dmul_rn(__dadd_rn(ssr, st.dw), c);
+    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(d, st.a[ks1[p]]), st.a[ks2[p]]));
+  }
+  K[s] = acc;
+}
+
+__device__ __forceinline__ double c_of(const gn_kkt_state &st, double ssr) {
+  return 1.0 / __dadd_rn(__dmul_rn(st.dc, ssr), __dadd_rn(1.0, __dmul_rn(st.dc, st.dw)));
+}
+
+// m-side of the condensed rhs: qs, qy and u = C qs + D qy
+__global__ void rhs_rows_kernel(int64_t m, gn_kkt_state st, gn_vec7 pv, double *qs, double *qy, double *u) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i >= m) return;
+  const double q_s = __dsub_rn(__dadd_rn(pv.s[i], __dmul_rn(inv_or_zero(st.dsl[i]), pv.zsl[i])),
+                               __dmul_rn(inv_or_zero(st.dsu[i]), pv.zsu[i]));
+  const double q_y = pv.y[i];
+  const double c = c_of(st, st.ss[i]);
+  const double d = __dmul_rn(__dadd_rn(st.ss[i], st.dw), c);
+  qs[i] = q_s;
+  qy[i] = q_y;
+  u[i] = __dadd_rn(__dmul_rn(c, q_s), __dmul_rn(d, q_y));
+}
+
+// n-side: qx and rhs = qx + A^T u
+__global__ void rhs_cols_kernel(int64_t n, const int64_t *ptr, const int32_t *pp, const int32_t *row,
+                                gn_kkt_state st, gn_vec7 pv, const double *u, double *qx, double *rhs) {
+  int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (j >= n) return;
+  const double q_x = __dsub_rn(__dadd_rn(pv.x[j], __dmul_rn(inv_or_zero(st.dxl[j]), pv.zxl[j])),
+                               __dmul_rn(inv_or_zero(st.dxu[j]), pv.zxu[j]));
+  double acc = 0.0;
+  for (int64_t t = ptr[j]; t < ptr[j + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(st.a[pp[t]], u[row[t]]));
+  qx[j] = q_x;
+  rhs[j] = __dadd_rn(q_x, acc);
+}
+
+__global__ void recover_sd_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, gn_kkt_state st,
+                                  const double *dx, const double *qs, const double *qy, double *ds,
+                                  double *dy) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i >= m) return;
+  double ax = 0.0;
+  for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) ax = __dadd_rn(ax, __dmul_rn(st.a[p], dx[col[p]]));
+  const double c = c_of(st, st.ss[i]);
+  const double dsi = __dmul_rn(c, __dsub_rn(__dadd_rn(ax, __dmul_rn(st.dc, qs[i])), qy[i]));
+  ds[i] = dsi;
+  dy[i] = __dsub_rn(__dmul_rn(__dadd_rn(st.ss[i], st.dw), dsi), qs[i]);
+}
+
+__global__ void recover_bd_kernel(int64_t len, const double *dl, const double *du, const double *zl,
+                                  const double *zu, const double *pzl, const double *pzu, const double *dv,
+                                  double *dzl, double *dzu, int32_t *flags) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i >= len) return;
+  const double wl = dl[i], wu = du[i];
+  if ((isfinite(wl) && !(wl > 0.0)) || (isfinite(wu) && !(wu > 0.0))) atomicOr(flags, 1);
+  dzl[i] = __dmul_rn(inv_or_zero(wl), __dsub_rn(pzl[i], __dmul_rn(zl[i], dv[i])));
+  dzu[i] = __dmul_rn(inv_or_zero(wu), __dadd_rn(pzu[i], __dmul_rn(zu[i], dv[i])));
+}
+
+// x-side residual blocks in double-double: rx, rzxl, rzxu (kkt.py:199-206)
+__global__ void residual_x_kernel(int64_t n, const int64_t *wptr, const int32_t *wp, const int32_t *wj,
+                                  const int64_t *atptr, const int32_t *atp, const int32_t *atrow,
+                                  gn_kkt_state st, gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs) {
+  double vmax[1] = {0.0};
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * kT) {
+    const double dxj = step.x[j];
+    dd wv = {0.0, 0.0};
+    for (int64_t t = wptr[j]; t < wptr[j + 1]; ++t) wv = dd_add(wv, dd_prod(st.w[wp[t]], step.x[wj[t]]));
+    dd atv = {0.0, 0.0};
+    for (int64_t t = atptr[j]; t < atptr[j + 1]; ++t) atv = dd_add(atv, dd_prod(st.a[atp[t]], step.y[atrow[t]]));
+    dd rx = dd_from(pv.x[j]);
+    rx = dd_add(rx, dd_neg(wv));
+    rx = dd_add(rx, dd_neg(dd_prod(st.dw, dxj)));
+    rx = dd_add(rx, dd_neg(atv));
+    rx = dd_add(rx, dd_from(step.zxl[j]));
+    rx = dd_add(rx, dd_from(-step.zxu[j]));
+    const double wl = st.dxl[j], wu = st.dxu[j];
+    dd rl = dd_add(dd_from(pv.zxl[j]), dd_neg(dd_prod(st.zxl[j], dxj)));
+    rl = dd_add(rl, dd_neg(dd_prod(isfinite(wl) ? wl : 1.0, step.zxl[j])));
+    dd ru = dd_add(dd_from(pv.zxu[j]), dd_prod(st.zxu[j], dxj));
+    ru = dd_add(ru, dd_neg(dd_prod(isfinite(wu) ? wu : 1.0, step.zxu[j])));
+    const double a = dd_round(rx), b = dd_round(rl), c = dd_round(ru);
+    res.x[j] = a;
+    res.zxl[j] = b;
+    res.zxu[j] = c;
+    double mx = fmax(fmax(fabs(a), fabs(b)), fabs(c));
+    if (a != a || b != b || c != c) mx = a + b + c;
+    vmax[0] = red_combine(RED_MAX, vmax[0], mx);
+  }
+  grid_reduce<1>(rs, vmax);
+}
+
+// s/y-side residual blocks: rs, ry, rzsl, rzsu (kkt.py:202-208)
+__global__ void residual_s_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, gn_kkt_state st,
+                                  gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs) {
+  double vmax[1] = {0.0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * kT) {
+    const double dsi = step.s[i], dyi = step.y[i];
+    dd ax = {0.0, 0.0};
+    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) ax = dd_add(ax, dd_prod(st.a[p], step.x[col[p]]));
+    dd r_s = dd_add(dd_from(pv.s[i]), dd_neg(dd_prod(st.dw, dsi)));
+    r_s = dd_add(r_s, dd_from(dyi));
+    r_s = dd_add(r_s, dd_from(step.zsl[i]));
+    r_s = dd_add(r_s, dd_from(-step.zsu[i]));
+    dd r_y = dd_add(dd_from(pv.y[i]), dd_neg(ax));
+    r_y = dd_add(r_y, dd_from(dsi));
+    r_y = dd_add(r_y, dd_prod(st.dc, dyi));
+    const double wl = st.dsl[i], wu = st.dsu[i];
+    dd rl = dd_add(dd_from(pv.zsl[i]), dd_neg(dd_prod(st.zsl[i], dsi)));
+    rl = dd_add(rl, dd_neg(dd_prod(isfinite(wl) ? wl : 1.0, step.zsl[i])));
+    dd ru = dd_add(dd_from(pv.zsu[i]), dd_prod(st.zsu[i], dsi));
+    ru = dd_add(ru, dd_neg(dd_prod(isfinite(wu) ? wu : 1.0, step.zsu[i])));
+    const double a = dd_round(r_s), b = dd_round(r_y), c = dd_round(rl), e = dd_round(ru);
+    res.s[i] = a;
+    res.y[i] = b;
+    res.zsl[i] = c;
+    res.zsu[i] = e;
+    double mx = fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(e)));
+    if (a != a || b != b || c != c || e != e) mx = a + b + c + e;
+    vmax[0] = red_combine(RED_MAX, vmax[0], mx);
+  }
+  grid_reduce<1>(rs, vmax);
+}
+
+__global__ void max2_kernel(const double *a, const double *b, double *out) {
+  double x = *a, y = *b;
+  *out = (x != x) ? x : ((y != y) ? y : fmax(x, y));
+}
+
+// max over |w|, |a|, |Sigma|, |z|, finite widths (kkt.py:211-221)
+__global__ void matrix_scale_kernel(int64_t n, int64_t m, int64_t nh, int64_t nj, gn_kkt_state st, RedSpec rs) {
+  double v[1] = {1.0};
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  double acc = fmax(1.0, fmax(st.dw, st.dc));
+  for (int64_t t = t0; t < nh; t += stride) acc = fmax(acc, fabs(st.w[t]));
+  for (int64_t t = t0; t < nj; t += stride) acc = fmax(acc, fabs(st.a[t]));
+  for (int64_t t = t0; t < n; t += stride) {
+    acc = fmax(acc, fmax(fabs(st.sx[t]), fmax(fabs(st.zxl[t]), fabs(st.zxu[t]))));
+    if (isfinite(st.dxl[t])) acc = fmax(acc, st.dxl[t]);
+    if (isfinite(st.dxu[t])) acc = fmax(acc, st.dxu[t]);
+  }
+  for (int64_t t = t0; t < m; t += stride) {
+    acc = fmax(acc, fmax(fabs(st.ss[t]), fmax(fabs(st.zsl[t]), fabs(st.zsu[t]))));
+    if (isfinite(st.dsl[t])) acc = fmax(acc, st.dsl[t]);
+    if (isfinite(st.dsu[t])) acc = fmax(acc, st.dsu[t]);
+  }
+  v[0] = acc;
+  grid_reduce<1>(rs, v);
+}
+
+__global__ void axpy7_kernel(int64_t n, int64_t m, gn_vec7 y, gn_vec7 x, double alpha) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (i < n) {
+    y.x[i] += alpha * x.x[i];
+    y.zxl[i] += alpha * x.zxl[i];
+    y.zxu[i] += alpha * x.zxu[i];
+  }
+  if (i < m) {
+    y.s[i] += alpha * x.s[i];
+    y.y[i] += alpha * x.y[i];
+    y.zsl[i] += alpha * x.zsl[i];
+    y.zsu[i] += alpha * x.zsu[i];
+  }
+}
+
+RedSpec max_spec(Kkt &K, double *out) {
+  RedSpec r{};
+  r.k = 1;
+  r.op[0] = RED_MAX;
+  r.out = out;
+  r.partials = K.d.partials;
+  r.counter = K.d.counter;
+  return r;
+}
+
+}  // namespace
+
+static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *hr, const int64_t *hc,
+                       int64_t nj, const int64_t *jr, const int64_t *jc, const Condense *cs) {
+  K.n = n;
+  K.m = m;
+  K.nh = nh;
+  K.nj = nj;
+  // A rows (jac is row-major sorted)
+  std::vector<int64_t> rowptr(m + 1, 0);
+  for (int64_t p = 0; p < nj; ++p) {
+    GN_REQUIRE(jr[p] >= 0 && jr[p] < m && jc[p] >= 0 && jc[p] < n, "Jacobian index out of range");
+    GN_REQUIRE(p == 0 || jr[p] >= jr[p - 1], "Jacobian must be sorted by row");
+    rowptr[jr[p] + 1]++;
+  }
+  for (int64_t i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
+  std::vector<int32_t> col(nj), at_p(nj), at_row(nj);
+  for (int64_t p = 0; p < nj; ++p) col[p] = static_cast<int32_t>(jc[p]);
+  std::vector<int64_t> atptr(n + 1, 0);
+  for (int64_t p = 0; p < nj; ++p) atptr[jc[p] + 1]++;
+  for (int64_t j = 0; j < n; ++j) atptr[j + 1] += atptr[j];
+  {
+    std::vector<int64_t> fl(atptr.begin(), atptr.end() - 1);
+    for (int64_t p = 0; p < nj; ++p) {
+      int64_t q = fl[jc[p]]++;
+      at_p[q] = static_cast<int32_t>(p);
+      at_row[q] = static_cast<int32_t>(jr[p]);
+    }
+  }
+  // W symmetric gather: pass 1 rows (all entries), pass 2 mirrored off-diagonals
+  std::vector<int64_t> wptr(n + 1, 0);
+  for (int64_t p = 0; p < nh; ++p) {
+    GN_REQUIRE(hr[p] >= 0 && hr[p] < n && hc[p] >= 0 && hc[p] <= hr[p], "Hessian index out of range");
+    wptr[hr[p] + 1]++;
+    if (hr[p] != hc[p]) wptr[hc[p] + 1]++;
+  }
+  for (int64_t i = 0; i < n; ++i) wptr[i + 1] += wptr[i];
+  std::vector<int32_t> wp(wptr[n]), wj(wptr[n]);
+  {
+    std::vector<int64_t> fl(wptr.begin(), wptr.end() - 1);
+    for (int64_t p = 0; p < nh; ++p) {
+      int64_t q = fl[hr[p]]++;
+      wp[q] = static_cast<int32_t>(p);
+      wj[q] = static_cast<int32_t>(hc[p]);
+    }
+    for (int64_t p = 0; p < nh; ++p)
+      if (hr[p] != hc[p]) {
+        int64_t q = fl[hc[p]]++;
+        wp[q] = static_cast<int32_t>(p);
+        wj[q] = static_cast<int32_t>(hr[p]);
+      }
+  }
+  K.d.a_rowptr = dev_upload(rowptr);
+  K.d.a_col = dev_upload(col);
+  K.d.at_ptr = dev_upload(atptr);
+  K.d.at_p = dev_upload(at_p);
+  K.d.at_row = dev_upload(at_row);
+  K.d.w_ptr = dev_upload(wptr);
+  K.d.w_p = dev_upload(wp);
+  K.d.w_j = dev_upload(wj);
+  K.d.partials = dev_alloc<double>(kRedMaxBlocks * kRedMaxSlots);
+  K.d.counter = dev_alloc<unsigned int>(1);
+  GN_CUDA(cudaMemset(K.d.counter, 0, sizeof(unsigned int)));
+  K.d.scratch = dev_alloc<double>(m > 0 ? m : 1);
+  if (cs) {
+    GN_REQUIRE(cs->n == n && cs->nnz_h == nh && cs->nnz_j == nj, "condensed structure mismatch");
+    const int64_t nk = static_cast<int64_t>(cs->indices.size());
+    const int64_t np = static_cast<int64_t>(cs->ata_map.size());
+    K.nk = nk;
+    std::vector<int32_t> kw(nk, -1), kd(nk, -1);
+    for (int64_t p = 0; p < nh; ++p) {
+      GN_REQUIRE(kw[cs->w_map[p]] == -1, "duplicate W entry in a K slot");
+      kw[cs->w_map[p]] = static_cast<int32_t>(p);
+    }
+    for (int64_t i = 0; i < n; ++i) kd[cs->diag_map[i]] = static_cast<int32_t>(i);
+    std::vector<int64_t> kp(nk + 1, 0);
+    for (int64_t p = 0; p < np; ++p) kp[cs->ata_map[p] + 1]++;
+    for (int64_t s = 0; s < nk; ++s) kp[s + 1] += kp[s];
+    std::vector<int32_t> krow(np), k1(np), k2(np);
+    std::vector<int64_t> fl(kp.begin(), kp.end() - 1);
+    for (int64_t p = 0; p < np; ++p) {
+      int64_t q = fl[cs->ata_map[p]]++;
+      krow[q] = static_cast<int32_t>(cs->ata_row[p]);
+      k1[q] = static_cast<int32_t>(cs->ata_s1[p]);
+      k2[q] = static_cast<int32_t>(cs->ata_s2[p]);
+    }
+    K.d.k_ptr = dev_upload(kp);
+    K.d.k_row = dev_upload(krow);
+    K.d.k_s1 = dev_upload(k1);
+    K.d.k_s2 = dev_upload(k2);
+    K.d.k_w = dev_upload(kw);
+    K.d.k_diag = dev_upload(kd);
+    K.has_assembly = true;
+  }
+}
+
+}  // namespace gn
+
+using namespace gn;
+
+#define ST(s) static_cast<cudaStream_t>(s)
+
+extern "C" int gn_kkt_create(int64_t n, int64_t m, int64_t nh, const int64_t *hr, const int64_t *hc,
+                             int64_t nj, const int64_t *jr, const int64_t *jc, const gn_condense *cs,
+                             gn_kkt **out) {
+  return guarded([&] {
+    auto *K = new gn_kkt();
+    try {
+      kkt_create(*K, n, m, nh, hr, hc, nj, jr, jc, cs);
+    } catch (...) {
+      delete K;
+      throw;
+    }
+    *out = K;
+  });
+}
+
+extern "C" void gn_kkt_destroy(gn_kkt *K) { delete K; }
+
+extern "C" int gn_kkt_sigma(int64_t len, const double *dl, const double *du, const double *zl,
+                            const double *zu, double *sigma, void *stream) {
+  return guarded([&] {
+    if (len == 0) return;
+    sigma_kernel<<<blocks_for(len), kT, 0, ST(stream)>>>(len, dl, du, zl, zu, sigma);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_matvec(gn_kkt *K, int kind, const double *vals, const double *v, double *out,
+                             void *stream) {
+  return guarded([&] {
+    if (kind == 0 && K->n)
+      w_matvec_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, vals, v, out);
+    else if (kind == 1 && K->m)
+      a_matvec_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, vals, v, out);
+    else if (kind == 2 && K->n)
+      at_matvec_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, vals, v, out);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_assemble(gn_kkt *K, const gn_kkt_state *st, double *kvals, void *stream) {
+  return guarded([&] {
+    GN_REQUIRE(K->has_assembly, "KKT plan built without the condensed structure");
+    if (K->nk == 0) return;
+    assemble_kernel<<<blocks_for(K->nk), kT, 0, ST(stream)>>>(K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1, K->d.k_s2,
+                                                            K->d.k_w, K->d.k_diag, *st, kvals);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_condense_rhs(gn_kkt *K, const gn_kkt_state *st, const gn_vec7 *pv, double *qx,
+                                   double *qs, double *qy, double *rhs, void *stream) {
+  return guarded([&] {
+    if (K->m)
+      rhs_rows_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, *st, *pv, qs, qy, K->d.scratch);
+    if (K->n)
+      rhs_cols_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *st, *pv,
+                                                             K->d.scratch, qx, rhs);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_recover_slack_dual(gn_kkt *K, const gn_kkt_state *st, const double *dx,
+                                         const double *qs, const double *qy, double *ds, double *dy,
+                                         void *stream) {
+  return guarded([&] {
+    if (K->m)
+      recover_sd_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, *st, dx, qs, qy,
+                                                               ds, dy);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_recover_bound_duals(gn_kkt *K, const gn_kkt_state *st, const double *dx,
+                                          const double *ds, const gn_vec7 *pv, double *dzxl, double *dzxu,
+                                          double *dzsl, double *dzsu, int32_t *flags, void *stream) {
+  return guarded([&] {
+    if (K->n)
+      recover_bd_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, st->dxl, st->dxu, st->zxl, st->zxu, pv->zxl,
+                                                               pv->zxu, dx, dzxl, dzxu, flags);
+    if (K->m)
+      recover_bd_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, st->dsl, st->dsu, st->zsl, st->zsu, pv->zsl,
+                                                               pv->zsu, ds, dzsl, dzsu, flags);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_residual(gn_kkt *K, const gn_kkt_state *st, const gn_vec7 *steps, const gn_vec7 *pv,
+                               gn_vec7 *res, double *norm, void *stream) {
+  return guarded([&] {
+    // norm[0..2): per-side maxima, combined into norm[0]
+    RedSpec rx = max_spec(*K, norm);
+    if (K->n)
+      residual_x_kernel<<<red_grid(K->n), kRedThreads, 0, ST(stream)>>>(K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, K->d.at_ptr,
+                                                               K->d.at_p, K->d.at_row, *st, *steps, *pv, *res, rx);
+    else
+      GN_CUDA(cudaMemsetAsync(norm, 0, sizeof(double), ST(stream)));
+    RedSpec rs = max_spec(*K, norm + 1);
+    if (K->m)
+      residual_s_kernel<<<red_grid(K->m), kRedThreads, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, *st, *steps, *pv,
+                                                               *res, rs);
+    else
+      GN_CUDA(cudaMemsetAsync(norm + 1, 0, sizeof(double), ST(stream)));
+    max2_kernel<<<1, 1, 0, ST(stream)>>>(norm, norm + 1, norm);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_matrix_scale(gn_kkt *K, const gn_kkt_state *st, double *out, void *stream) {
+  return guarded([&] {
+    int64_t big = std::max(std::max(K->n, K->m), std::max(K->nh, K->nj));
+    RedSpec r = max_spec(*K, out);
+    matrix_scale_kernel<<<red_grid(big, 4), kRedThreads, 0, ST(stream)>>>(K->n, K->m, K->nh, K->nj, *st, r);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_vec7_axpy(gn_kkt *K, gn_vec7 *y, const gn_vec7 *x, double alpha, void *stream) {
+  return guarded([&] {
+    int64_t len = std::max(K->n, K->m);
+    if (len == 0) return;
+    axpy7_kernel<<<blocks_for(len), kT, 0, ST(stream)>>>(K->n, K->m, *y, *x, alpha);
+    GN_LAUNCH_CHECK();
+  });
+}

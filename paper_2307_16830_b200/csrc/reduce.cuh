@@ -1,0 +1,83 @@
+// Deterministic grid-wide reductions: per-CTA partials reduced by the last
+// CTA to finish, in CTA-index order (bitwise reproducible sums; max/min
+// exact), no floating-point atomics.
+#pragma once
+
+#include <cfloat>
+
+#include "device.cuh"
+
+namespace gn {
+
+enum RedOp : int { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
+
+constexpr int kRedThreads = 256;
+constexpr int kRedMaxBlocks = 296;   // 2 CTAs per SM on 148 SMs
+constexpr int kRedMaxSlots = 24;
+
+struct RedSpec {
+  int k;                      // number of reduced quantities
+  int op[kRedMaxSlots];       // RedOp per slot
+  double *out;                // k outputs (device)
+  double *partials;           // kRedMaxBlocks * kRedMaxSlots scratch
+  unsigned int *counter;      // zero-initialised; reset by the last CTA
+};
+
+__device__ __forceinline__ double red_identity(int op) {
+  return op == RED_SUM ? 0.0 : (op == RED_MAX ? -DBL_MAX : DBL_MAX);
+}
+
+__device__ __forceinline__ double red_combine(int op, double a, double b) {
+  if (op == RED_SUM) return a + b;
+  if (a != a) return a;  // NaN propagates like numpy's max/min
+  if (b != b) return b;
+  if (op == RED_MAX) return b > a ? b : a;
+  return b < a ? b : a;
+}
+
+inline int red_grid(int64_t n, int per_thread = 1) {
+  int64_t g = (n + static_cast<int64_t>(kRedThreads) * per_thread - 1) / (kRedThreads * per_thread);
+  if (g < 1) g = 1;
+  if (g > kRedMaxBlocks) g = kRedMaxBlocks;
+  return static_cast<int>(g);
+}
+
+// Reduce `vals[0..K)` held by every thread of the grid; thread 0 of the last
+// CTA writes spec.out.  Must be called by all threads of every CTA.
+template <int K>
+__device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
+  __shared__ double sh[K][kRedThreads / 32];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double v = vals[k];
+    for (int o = 16; o > 0; o >>= 1) v = red_combine(spec.op[k], v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) sh[k][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double v = sh[k][0];
+      for (int w = 1; w < nw; ++w) v = red_combine(spec.op[k], v, sh[k][w]);
+      spec.partials[blockIdx.x * kRedMaxSlots + k] = v;
+    }
+    __threadfence();
+    unsigned int done = atomicAdd(spec.counter, 1u);
+    last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double v = __ldcg(spec.partials + k);
+      for (unsigned b = 1; b < gridDim.x; ++b) v = red_combine(spec.op[k], v, __ldcg(spec.partials + b * kRedMaxSlots + k));
+      spec.out[k] = v;
+    }
+    *spec.counter = 0u;
+  }
+}
+
+}  // namespace gn

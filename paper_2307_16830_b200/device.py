@@ -1,0 +1,46 @@
+"""Device plumbing: the CUDA device, streams and tensor helpers (torch)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+
+class DeviceUnavailable(RuntimeError):
+    """Raised when a device entry point runs without a CUDA device."""
+
+
+def require_cuda() -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceUnavailable(
+            "the condensed-space solve path runs on the GPU only (no CPU fallback); "
+            "no CUDA device is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def to_dev(a, dtype=torch.float64):
+    """numpy / list / tensor -> contiguous CUDA tensor of ``dtype``."""
+    dev = require_cuda()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev)
+
+
+def empty(n, dtype=torch.float64):
+    return torch.empty(int(n), dtype=dtype, device=require_cuda())
+
+
+def zeros(n, dtype=torch.float64):
+    return torch.zeros(int(n), dtype=dtype, device=require_cuda())
+
+
+def is_tensor(a) -> bool:
+    return isinstance(a, torch.Tensor)
+
+
+def to_host(t) -> np.ndarray:
+    return t.detach().cpu().numpy()

@@ -1,0 +1,403 @@
+"""Condensed KKT machinery on the GPU.
+
+Same structure and API as reference src/gridnlp/kkt.py: the seven-block
+Newton system, its condensation to
+
+    (W + dw I + Sigma_x + A^T D A) dx = qx + A^T (C qs + D qy),
+    C = (dc Sigma_s + (1 + dc dw) I)^-1,  D = (Sigma_s + dw I) C,
+
+diagonal recoveries, the inertia-correction schedule and iterative
+refinement against the full system.  Every vector lives in HBM; the
+arithmetic runs in the native kernels of ``csrc/kkt.cu`` (assembly, rhs,
+recoveries, double-double residual) and ``csrc/chol.cu`` (factor/solve).
+Host code only sequences kernels and reads back the scalars the control
+flow branches on (PD flag, residual norms).
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import device as D
+from . import sparse as S
+
+DELTA_W_INIT = 1e-4
+DELTA_W_MIN = 1e-20
+DELTA_W_MAX = 1e40
+DELTA_C_VALUE = 1e-8
+KAPPA_IR = 10.0
+MAX_IR_ROUNDS = 10
+
+FIELDS = ("x", "s", "y", "zxl", "zxu", "zsl", "zsu")
+
+
+class DegenerateInterior(RuntimeError):
+    """A finite-bound slack is not strictly positive."""
+
+
+class RegularizationExhausted(RuntimeError):
+    """No positive-definite condensed system below the delta_w ceiling."""
+
+
+@dataclass
+class RegState:
+    delta_w_last: float = 0.0
+
+
+class _Vec7:
+    """Seven device vectors (x, s, y, zxl, zxu, zsl, zsu)."""
+
+    def __init__(self, x, s, y, zxl, zxu, zsl, zsu):
+        self.x, self.s, self.y = D.to_dev(x), D.to_dev(s), D.to_dev(y)
+        self.zxl, self.zxu = D.to_dev(zxl), D.to_dev(zxu)
+        self.zsl, self.zsu = D.to_dev(zsl), D.to_dev(zsu)
+
+    @classmethod
+    def empty(cls, n, m):
+        obj = cls.__new__(cls)
+        for f, k in zip(FIELDS, (n, m, m, n, n, m, m)):
+            setattr(obj, f, D.empty(k))
+        return obj
+
+    def parts(self):
+        return [getattr(self, f) for f in FIELDS]
+
+    def c_struct(self) -> L.Vec7:
+        return L.Vec7(*(t.data_ptr() for t in self.parts()))
+
+    def numpy(self):
+        return [D.to_host(t) for t in self.parts()]
+
+
+class PVec(_Vec7):
+    """Right-hand side of the seven-block Newton system (kkt.py:60-70)."""
+
+
+class Steps(_Vec7):
+    """Newton steps (kkt.py:73-85)."""
+
+    def axpy(self, other: "Steps", alpha=1.0) -> None:
+        for f in FIELDS:
+            getattr(self, f).add_(getattr(other, f), alpha=alpha)
+
+
+def _bind(kkt, y: _Vec7, x: _Vec7, alpha):
+    yc, xc = y.c_struct(), x.c_struct()
+    L.check(L.lib().gn_vec7_axpy(kkt, ctypes.byref(yc), ctypes.byref(xc), alpha, D.stream_ptr()))
+
+
+@dataclass
+class CondensedStructure:
+    matrix: S.SparseSymmetric
+    w_map: np.ndarray
+    diag_map: np.ndarray
+    ata_map: np.ndarray
+    ata_row: np.ndarray
+    ata_s1: np.ndarray
+    ata_s2: np.ndarray
+    handle: object = None
+
+    def __del__(self):
+        if self.handle is not None and L._lib is not None:
+            L.lib().gn_condense_destroy(self.handle)
+            self.handle = None
+
+
+def symbolic_condense(hess_rows, hess_cols, jac_rows, jac_cols, n) -> CondensedStructure:
+    """Pattern of W + diag + tril(A^T A) plus scatter maps (kkt.py:243-283), natively."""
+    hr, hc, jr, jc = (L.i64(a) for a in (hess_rows, hess_cols, jac_rows, jac_cols))
+    h = ctypes.c_void_p()
+    L.check(L.lib().gn_condense_create(n, hr.size, L.ptr(hr), L.ptr(hc), jr.size, L.ptr(jr),
+                                       L.ptr(jc), ctypes.byref(h)))
+    nk, npr = ctypes.c_int64(), ctypes.c_int64()
+    L.check(L.lib().gn_condense_info(h, ctypes.byref(nk), ctypes.byref(npr)))
+    indptr, indices = np.empty(n + 1, np.int64), np.empty(nk.value, np.int64)
+    w_map, diag_map = np.empty(hr.size, np.int64), np.empty(n, np.int64)
+    ata = [np.empty(npr.value, np.int64) for _ in range(4)]
+    L.check(L.lib().gn_condense_export(h, L.ptr(indptr), L.ptr(indices), L.ptr(w_map),
+                                       L.ptr(diag_map), *(L.ptr(a) for a in ata)))
+    mat = S.SparseSymmetric(n, indptr, indices, np.zeros(nk.value))
+    return CondensedStructure(mat, w_map, diag_map, *ata, handle=h)
+
+
+class KKTWorkspace:
+    """Device values of the full KKT system at the current iterate (kkt.py:96-221)."""
+
+    def __init__(self, n, m, hess_rows, hess_cols, jac_rows, jac_cols, condensed=None):
+        self.n, self.m = int(n), int(m)
+        self.hess_rows, self.hess_cols = L.i64(hess_rows), L.i64(hess_cols)
+        self.jac_rows, self.jac_cols = L.i64(jac_rows), L.i64(jac_cols)
+        D.require_cuda()
+        h = ctypes.c_void_p()
+        L.check(L.lib().gn_kkt_create(self.n, self.m, self.hess_rows.size, L.ptr(self.hess_rows),
+                                      L.ptr(self.hess_cols), self.jac_rows.size, L.ptr(self.jac_rows),
+                                      L.ptr(self.jac_cols),
+                                      None if condensed is None else condensed.handle,
+                                      ctypes.byref(h)))
+        self.handle = h
+        self._has_assembly = condensed is not None
+        self.w_vals = D.zeros(self.hess_rows.size)
+        self.a_vals = D.zeros(self.jac_rows.size)
+        self.delta_w = 0.0
+        self.delta_c = 0.0
+        for f in ("dxl", "dxu", "zxl", "zxu", "sigma_x"):
+            setattr(self, f, D.zeros(self.n))
+        for f in ("dsl", "dsu", "zsl", "zsu", "sigma_s"):
+            setattr(self, f, D.zeros(self.m))
+        self.flags = torch.zeros(1, dtype=torch.int32, device=self.w_vals.device)
+        self._scal = D.zeros(4)
+
+    def attach_condensed(self, condensed: CondensedStructure):
+        """Rebuild the plan with the assembly maps of ``condensed``."""
+        if self._has_assembly:
+            return
+        L.lib().gn_kkt_destroy(self.handle)
+        h = ctypes.c_void_p()
+        L.check(L.lib().gn_kkt_create(self.n, self.m, self.hess_rows.size, L.ptr(self.hess_rows),
+                                      L.ptr(self.hess_cols), self.jac_rows.size, L.ptr(self.jac_rows),
+                                      L.ptr(self.jac_cols), condensed.handle, ctypes.byref(h)))
+        self.handle = h
+        self._has_assembly = True
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and L._lib is not None:
+            L.lib().gn_kkt_destroy(h)
+            self.handle = None
+
+    # -- state -------------------------------------------------------------
+    def set_iterate(self, w_vals, a_vals, dxl, dxu, zxl, zxu, dsl, dsu, zsl, zsu):
+        for name, v in (("w_vals", w_vals), ("a_vals", a_vals), ("dxl", dxl), ("dxu", dxu),
+                        ("zxl", zxl), ("zxu", zxu), ("dsl", dsl), ("dsu", dsu), ("zsl", zsl),
+                        ("zsu", zsu)):
+            dst = getattr(self, name)
+            if D.is_tensor(v) and v.data_ptr() == dst.data_ptr():
+                continue
+            dst.copy_(D.to_dev(v))
+        st = D.stream_ptr()
+        lib = L.lib()
+        L.check(lib.gn_kkt_sigma(self.n, *(L.ptr(t) for t in (self.dxl, self.dxu, self.zxl,
+                                                                self.zxu, self.sigma_x)), st))
+        L.check(lib.gn_kkt_sigma(self.m, *(L.ptr(t) for t in (self.dsl, self.dsu, self.zsl,
+                                                                self.zsu, self.sigma_s)), st))
+
+    def state(self) -> L.KktState:
+        return L.KktState(*(t.data_ptr() for t in (
+            self.w_vals, self.a_vals, self.dxl, self.dxu, self.dsl, self.dsu, self.zxl, self.zxu,
+            self.zsl, self.zsu, self.sigma_x, self.sigma_s)), float(self.delta_w), float(self.delta_c))
+
+    # -- matrix-vector products ----------------------------------------------
+    def _mv(self, kind, vals, v, n_out):
+        out = D.empty(n_out)
+        v = D.to_dev(v)
+        L.check(L.lib().gn_kkt_matvec(self.handle, kind, L.ptr(vals), L.ptr(v), L.ptr(out),
+                                      D.stream_ptr()))
+        return out
+
+    def w_matvec(self, v):
+        return self._mv(0, self.w_vals, v, self.n)
+
+    def a_matvec(self, v):
+        return self._mv(1, self.a_vals, v, self.m)
+
+    def at_matvec(self, u):
+        return self._mv(2, self.a_vals, u, self.n)
+
+    # -- condensation formulas (convenience; the solver uses fused kernels) ---
+    def c_diag(self):
+        return 1.0 / (self.delta_c * self.sigma_s + (1.0 + self.delta_c * self.delta_w))
+
+    def d_diag(self):
+        return (self.sigma_s + self.delta_w) * self.c_diag()
+
+    def condense_pvec(self, pv: PVec):
+        qx, qs, qy, _ = self._condense(pv)
+        return qx, qs, qy
+
+    def _condense(self, pv):
+        qx, rhs = D.empty(self.n), D.empty(self.n)
+        qs, qy = D.empty(self.m), D.empty(self.m)
+        st, pc = self.state(), pv.c_struct()
+        L.check(L.lib().gn_kkt_condense_rhs(self.handle, ctypes.byref(st), ctypes.byref(pc),
+                                            L.ptr(qx), L.ptr(qs), L.ptr(qy), L.ptr(rhs),
+                                            D.stream_ptr()))
+        return qx, qs, qy, rhs
+
+    def condensed_rhs(self, qx, qs, qy):
+        z_n, z_m = D.zeros(self.n), D.zeros(self.m)
+        return self._condense(PVec(qx, qs, qy, z_n, z_n, z_m, z_m))[3]
+
+    def recover_slack_dual(self, dx, qx, qs, qy):
+        ds, dy = D.empty(self.m), D.empty(self.m)
+        st = self.state()
+        L.check(L.lib().gn_kkt_recover_slack_dual(self.handle, ctypes.byref(st), L.ptr(D.to_dev(dx)),
+                                                  L.ptr(D.to_dev(qs)), L.ptr(D.to_dev(qy)), L.ptr(ds),
+                                                  L.ptr(dy), D.stream_ptr()))
+        return ds, dy
+
+    def recover_bound_duals(self, dx, ds, pv: PVec, check=True):
+        out = [D.empty(k) for k in (self.n, self.n, self.m, self.m)]
+        st, pc = self.state(), pv.c_struct()
+        if check:
+            self.flags.zero_()
+        L.check(L.lib().gn_kkt_recover_bound_duals(
+            self.handle, ctypes.byref(st), L.ptr(D.to_dev(dx)), L.ptr(D.to_dev(ds)), ctypes.byref(pc),
+            *(L.ptr(t) for t in out), L.ptr(self.flags), D.stream_ptr()))
+        if check and int(self.flags.item()) & 1:
+            raise DegenerateInterior("non-positive bound slack at an interior iterate")
+        return tuple(out)
+
+    # -- full seven-block system ----------------------------------------------
+    def residual_full(self, st_: Steps, pv: PVec, norm_out=None):
+        """pv - M_full * steps, accumulated in double-double (kkt.py:190-209)."""
+        res = PVec.empty(self.n, self.m)
+        st, sc, pc, rc = self.state(), st_.c_struct(), pv.c_struct(), res.c_struct()
+        norm = norm_out if norm_out is not None else self._scal[0:2]
+        L.check(L.lib().gn_kkt_residual(self.handle, ctypes.byref(st), ctypes.byref(sc),
+                                        ctypes.byref(pc), ctypes.byref(rc), L.ptr(norm),
+                                        D.stream_ptr()))
+        res._norm = norm
+        return res
+
+    def matrix_scale_device(self, out):
+        st = self.state()
+        L.check(L.lib().gn_kkt_matrix_scale(self.handle, ctypes.byref(st), L.ptr(out), D.stream_ptr()))
+        return out
+
+    def matrix_scale(self) -> float:
+        return float(self.matrix_scale_device(self._scal[2:3]).item())
+
+
+def residual_norm(pv) -> float:
+    """max |block| over the seven blocks (kkt.py:224-229)."""
+    nrm = getattr(pv, "_norm", None)
+    if nrm is not None:
+        return float(nrm[0].item())
+    out = 0.0
+    for t in pv.parts():
+        if t.numel():
+            out = max(out, float(t.abs().max().item()))
+    return out
+
+
+class CondensedBackend:
+    """Sparse Cholesky of the condensed primal system on the GPU (kkt.py:286-325)."""
+
+    def __init__(self, ws: KKTWorkspace, ordering=None):
+        self.ws = ws
+        self.structure = symbolic_condense(ws.hess_rows, ws.hess_cols, ws.jac_rows, ws.jac_cols, ws.n)
+        ws.attach_condensed(self.structure)
+        if ordering is None:
+            ordering = S.amd_order(self.structure.matrix)
+        self.symbolic = S.symbolic_cholesky(self.structure.matrix, ordering)
+        self.symbolic.handle()
+        self.kvals = D.zeros(self.structure.matrix.nnz)
+        self.structure.matrix.values = self.kvals
+        self.fws = S.FactorWorkspace(self.symbolic)
+        self.factor = None
+        self.n_factorizations = 0
+        self._dx = D.empty(ws.n)
+
+    def assemble(self) -> None:
+        st = self.ws.state()
+        L.check(L.lib().gn_kkt_assemble(self.ws.handle, ctypes.byref(st), L.ptr(self.kvals),
+                                        D.stream_ptr()))
+
+    def factorize_async(self):
+        self.assemble()
+        self.n_factorizations += 1
+        self.factor = S.factorize_device(self.symbolic, self.kvals, self.fws)
+        return self.factor
+
+    def try_factorize(self) -> bool:
+        return self.factorize_async().ok
+
+    def solve3(self, qx, qs, qy):
+        ws = self.ws
+        rhs = ws.condensed_rhs(qx, qs, qy)
+        dx = S.solve_device(self.factor, rhs, D.empty(ws.n))
+        ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
+        return dx, ds, dy
+
+    def solve_pvec(self, pv: PVec):
+        """Fused condense_pvec + solve3 for the solver's hot path."""
+        ws = self.ws
+        qx, qs, qy, rhs = ws._condense(pv)
+        dx = S.solve_device(self.factor, rhs, D.empty(ws.n))
+        ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
+        return dx, ds, dy
+
+
+def solve_with_regularization(ws, backend, pv: PVec, reg: RegState):
+    """Factorize with the inertia-correction schedule, then solve (kkt.py:424-447)."""
+    ws.delta_w = 0.0
+    ws.delta_c = 0.0
+    if not backend.try_factorize():
+        had = reg.delta_w_last > 0.0
+        ws.delta_c = DELTA_C_VALUE
+        ws.delta_w = max(DELTA_W_MIN, reg.delta_w_last / 3.0) if had else DELTA_W_INIT
+        while not backend.try_factorize():
+            ws.delta_w *= 8.0 if had else 100.0
+            if ws.delta_w > DELTA_W_MAX:
+                raise RegularizationExhausted(
+                    f"delta_w exceeded {DELTA_W_MAX:g} without positive definiteness")
+        reg.delta_w_last = ws.delta_w
+    if hasattr(backend, "solve_pvec"):
+        dx, ds, dy = backend.solve_pvec(pv)
+    else:
+        qx, qs, qy = ws.condense_pvec(pv)
+        dx, ds, dy = backend.solve3(qx, qs, qy)
+    return (dx, ds, dy), ws.delta_w
+
+
+def assemble_steps(ws, pv: PVec, dx, ds, dy, check=True) -> Steps:
+    dz = ws.recover_bound_duals(dx, ds, pv, check=check)
+    st = Steps.__new__(Steps)
+    st.x, st.s, st.y = D.to_dev(dx), D.to_dev(ds), D.to_dev(dy)
+    st.zxl, st.zxu, st.zsl, st.zsu = dz
+    return st
+
+
+@dataclass
+class RefinementStats:
+    rounds: int = 0
+    initial_residual: float = 0.0
+    final_residual: float = 0.0
+    scale: float = 1.0
+
+    @property
+    def relative_residual(self) -> float:
+        return self.final_residual / self.scale
+
+
+def iterative_refinement(ws, backend, steps: Steps, pv: PVec) -> RefinementStats:
+    """Refine against the full seven-block system in place (kkt.py:467-491).
+
+    The matrix scale and the first residual norm come back in one read.
+    """
+    scal = ws._scal
+    ws.matrix_scale_device(scal[2:3])
+    res = ws.residual_full(steps, pv, norm_out=scal[0:2])
+    host = scal[0:3].cpu().numpy()
+    scale, rnorm = float(host[2]), float(host[0])
+    target = KAPPA_IR * np.finfo(float).eps * scale
+    stats = RefinementStats(initial_residual=rnorm, final_residual=rnorm, scale=scale)
+    while stats.final_residual > target and stats.rounds < MAX_IR_ROUNDS:
+        dx, ds, dy = backend.solve_pvec(res)
+        corr = assemble_steps(ws, res, dx, ds, dy, check=False)
+        _bind(ws.handle, steps, corr, 1.0)
+        res = ws.residual_full(steps, pv, norm_out=scal[0:2])
+        new = float(scal[0].item())
+        stats.rounds += 1
+        if new >= stats.final_residual:
+            _bind(ws.handle, steps, corr, -1.0)
+            break
+        enough = new <= stats.final_residual / 2.0
+        stats.final_residual = new
+        if not enough:
+            break
+    return stats
