@@ -212,6 +212,61 @@ int gn_kkt_matrix_scale(gn_kkt *k, const gn_kkt_state *st, double *out, void *st
 /* y += alpha x over all seven blocks (Steps.axpy, kkt.py:83-85) */
 int gn_vec7_axpy(gn_kkt *k, gn_vec7 *y, const gn_vec7 *x, double alpha, void *stream);
 
+/* ------------------------------------------------------------------ */
+/* Interior-point vector algebra (device)                              */
+/* ------------------------------------------------------------------ */
+
+/* Device vectors of one interior-point solve (ipm.py:326-548). */
+typedef struct gn_ipm_vecs {
+  double *x, *s, *y, *zxl, *zxu, *zsl, *zsu;   /* iterate                       */
+  const double *xl, *xu, *sl, *su;             /* bounds (+-inf when absent)     */
+  double *dxl, *dxu, *dsl, *dsu;               /* widths (+inf when absent)      */
+  double *sx, *ss;                             /* Sigma_x, Sigma_s               */
+  double *grad, *c, *jac;                      /* scaled AD outputs              */
+  double *dual_x, *dual_s, *primal;            /* KKT residual blocks            */
+} gn_ipm_vecs;
+
+/* layout of the scalar block written by gn_ipm_prep (device doubles) */
+#define GN_IPM_MAX_MU 16
+#define GN_PREP_X_DUAL 0     /* max |dual_x|                         */
+#define GN_PREP_X_ZL1 1      /* sum |zxl| + |zxu|                    */
+#define GN_PREP_X_LOGL 2     /* sum log dxl (finite)                 */
+#define GN_PREP_X_LOGU 3     /* sum log dxu (finite)                 */
+#define GN_PREP_X_COMP 4     /* [n_mu] max |z w - mu_k| (finite w)   */
+#define GN_PREP_S 24         /* start of the s-side block            */
+#define GN_PREP_S_DUAL 0     /* max |dual_s|                         */
+#define GN_PREP_S_PRIMAL 1   /* max |primal|                         */
+#define GN_PREP_S_ZL1 2      /* sum |zsl| + |zsu|                    */
+#define GN_PREP_S_YL1 3      /* sum |y|                              */
+#define GN_PREP_S_THETA 4    /* sum |g - s|                          */
+#define GN_PREP_S_LOGL 5
+#define GN_PREP_S_LOGU 6
+#define GN_PREP_S_COMP 7     /* [n_mu]                               */
+#define GN_PREP_DOUBLES 48
+
+/* widths, Sigma, dual_x = grad + A^T y - zxl + zxu, dual_s, primal and the
+ * reductions of kkt_residual / barrier_phi (ipm.py:150-157, 393-429) for
+ * the barrier candidates mus[0..n_mu) */
+int gn_ipm_prep(gn_kkt *k, const gn_ipm_vecs *v, int32_t n_mu, const double *mus_host,
+                double *scal, void *stream);
+/* seven-block right-hand side (ipm.py:434-442) */
+int gn_ipm_pvec(gn_kkt *k, const gn_ipm_vecs *v, double mu, gn_vec7 *pv, void *stream);
+/* scal[0..4) = (alpha_x, alpha_s, alpha_z, dphi): fraction-to-boundary and
+ * the barrier directional derivative (ipm.py:455-476) */
+int gn_ipm_direction(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double mu, double tau,
+                     double *scal, void *stream);
+/* xt = x + alpha dx, st = s + alpha ds (ipm.py:482-483) */
+int gn_ipm_trial_point(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
+                       double *xt, double *st, void *stream);
+/* scal[0..5) = (theta_t, log-sums of the four trial widths) (ipm.py:490-492);
+ * a non-positive finite width yields a NaN log-sum */
+int gn_ipm_trial_merit(gn_kkt *k, const gn_ipm_vecs *v, const double *ct, const double *xt,
+                       const double *st, double *scal, void *stream);
+/* accept the step, apply the kappa_sigma dual safeguard, flag (bit 2) lost
+ * interiority (ipm.py:521-548) */
+int gn_ipm_accept(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
+                  double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,18 @@ class Vec7(ctypes.Structure):
     _fields_ = [(f, P) for f in ("x", "s", "y", "zxl", "zxu", "zsl", "zsu")]
 
 
+class IpmVecs(ctypes.Structure):
+    _fields_ = [(f, P) for f in ("x", "s", "y", "zxl", "zxu", "zsl", "zsu", "xl", "xu", "sl", "su",
+                                 "dxl", "dxu", "dsl", "dsu", "sx", "ss", "grad", "c", "jac",
+                                 "dual_x", "dual_s", "primal")]
+
+
+# scalar-block layout of gn_ipm_prep (gridopf.h GN_PREP_*)
+IPM_MAX_MU = 16
+PREP_S = 24
+PREP_DOUBLES = 48
+
+
 class GridOpfError(RuntimeError):
     pass
 
@@ -78,6 +90,12 @@ _SIGS = {
     "gn_kkt_residual": (c_i32, [P, P, P, P, P, P, P]),
     "gn_kkt_matrix_scale": (c_i32, [P, P, P, P]),
     "gn_vec7_axpy": (c_i32, [P, P, P, c_dbl, P]),
+    "gn_ipm_prep": (c_i32, [P, P, c_i32, P, P, P]),
+    "gn_ipm_pvec": (c_i32, [P, P, c_dbl, P, P]),
+    "gn_ipm_direction": (c_i32, [P, P, P, c_dbl, c_dbl, P, P]),
+    "gn_ipm_trial_point": (c_i32, [P, P, P, c_dbl, P, P, P]),
+    "gn_ipm_trial_merit": (c_i32, [P, P, P, P, P, P, P]),
+    "gn_ipm_accept": (c_i32, [P, P, P, c_dbl, c_dbl, c_dbl, c_dbl, P, P]),
 }
 
 _lib = None

@@ -1,0 +1,288 @@
+// Interior-point vector algebra on the device (reference src/gridnlp/ipm.py:
+// 150-157 kkt_residual, 340-346 barrier_phi, 393-442 iterate prep and right-
+// hand side, 455-476 fraction-to-boundary and dphi, 482-492 trial merit,
+// 521-548 step acceptance with the kappa_sigma safeguard).
+//
+// The prep/direction/merit kernels fuse the elementwise work with every
+// reduction the host control flow branches on; each writes a small scalar
+// block that the driver reads back in one copy.
+#include <cmath>
+
+#include "reduce.cuh"
+
+namespace gn {
+namespace {
+
+__device__ __forceinline__ double inv0(double w) { return isfinite(w) ? 1.0 / w : 0.0; }
+__device__ __forceinline__ double width_lo(double v, double b) { return isfinite(b) ? v - b : INFINITY; }
+__device__ __forceinline__ double width_hi(double v, double b) { return isfinite(b) ? b - v : INFINITY; }
+
+struct MuList {
+  int n;
+  double mu[GN_IPM_MAX_MU];
+};
+
+RedSpec spec(Kkt &K, double *out, int k, const int *ops) {
+  RedSpec r{};
+  r.k = k;
+  for (int i = 0; i < k; ++i) r.op[i] = ops[i];
+  r.out = out;
+  r.partials = K.d.partials;
+  r.counter = K.d.counter;
+  return r;
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+prep_x_kernel(int64_t n, const int64_t *atptr, const int32_t *atp, const int32_t *atrow, gn_ipm_vecs v,
+              MuList mus, RedSpec rs) {
+  double acc[4 + GN_IPM_MAX_MU];
+  acc[0] = 0.0;
+  acc[1] = 0.0;
+  acc[2] = 0.0;
+  acc[3] = 0.0;
+  for (int k = 0; k < mus.n; ++k) acc[4 + k] = 0.0;
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; j < n;
+       j += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+    const double x = v.x[j];
+    const double wl = width_lo(x, v.xl[j]), wu = width_hi(x, v.xu[j]);
+    const double zl = v.zxl[j], zu = v.zxu[j];
+    v.dxl[j] = wl;
+    v.dxu[j] = wu;
+    v.sx[j] = __dadd_rn(__dmul_rn(zl, inv0(wl)), __dmul_rn(zu, inv0(wu)));
+    double aty = 0.0;
+    for (int64_t t = atptr[j]; t < atptr[j + 1]; ++t) aty += v.jac[atp[t]] * v.y[atrow[t]];
+    const double dx = ((v.grad[j] + aty) - zl) + zu;
+    v.dual_x[j] = dx;
+    acc[0] = red_combine(RED_MAX, acc[0], fabs(dx));
+    acc[1] += fabs(zl) + fabs(zu);
+    const bool fl = isfinite(wl), fu = isfinite(wu);
+    if (fl) acc[2] += log(wl);
+    if (fu) acc[3] += log(wu);
+    for (int k = 0; k < mus.n; ++k) {
+      double c = 0.0;
+      if (fl) c = fabs(zl * wl - mus.mu[k]);
+      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mus.mu[k]));
+      acc[4 + k] = red_combine(RED_MAX, acc[4 + k], c);
+    }
+  }
+  grid_reduce(rs, acc);
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+prep_s_kernel(int64_t m, gn_ipm_vecs v, MuList mus, RedSpec rs) {
+  double acc[7 + GN_IPM_MAX_MU];
+  for (int k = 0; k < 7 + mus.n; ++k) acc[k] = 0.0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+    const double s = v.s[i], y = v.y[i];
+    const double wl = width_lo(s, v.sl[i]), wu = width_hi(s, v.su[i]);
+    const double zl = v.zsl[i], zu = v.zsu[i];
+    v.dsl[i] = wl;
+    v.dsu[i] = wu;
+    v.ss[i] = __dadd_rn(__dmul_rn(zl, inv0(wl)), __dmul_rn(zu, inv0(wu)));
+    const double ds = (-y - zl) + zu;
+    const double pr = v.c[i] - s;
+    v.dual_s[i] = ds;
+    v.primal[i] = pr;
+    acc[0] = red_combine(RED_MAX, acc[0], fabs(ds));
+    acc[1] = red_combine(RED_MAX, acc[1], fabs(pr));
+    acc[2] += fabs(zl) + fabs(zu);
+    acc[3] += fabs(y);
+    acc[4] += fabs(pr);
+    const bool fl = isfinite(wl), fu = isfinite(wu);
+    if (fl) acc[5] += log(wl);
+    if (fu) acc[6] += log(wu);
+    for (int k = 0; k < mus.n; ++k) {
+      double c = 0.0;
+      if (fl) c = fabs(zl * wl - mus.mu[k]);
+      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mus.mu[k]));
+      acc[7 + k] = red_combine(RED_MAX, acc[7 + k], c);
+    }
+  }
+  grid_reduce(rs, acc);
+}
+
+__global__ void pvec_kernel(int64_t n, int64_t m, gn_ipm_vecs v, double mu, gn_vec7 pv) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double wl = v.dxl[i], wu = v.dxu[i];
+    pv.x[i] = -v.dual_x[i];
+    pv.zxl[i] = (isfinite(wl) ? mu : 0.0) - v.zxl[i] * (isfinite(wl) ? wl : 0.0);
+    pv.zxu[i] = (isfinite(wu) ? mu : 0.0) - v.zxu[i] * (isfinite(wu) ? wu : 0.0);
+  }
+  if (i < m) {
+    const double wl = v.dsl[i], wu = v.dsu[i];
+    pv.s[i] = -v.dual_s[i];
+    pv.y[i] = -v.primal[i];
+    pv.zsl[i] = (isfinite(wl) ? mu : 0.0) - v.zsl[i] * (isfinite(wl) ? wl : 0.0);
+    pv.zsu[i] = (isfinite(wu) ? mu : 0.0) - v.zsu[i] * (isfinite(wu) ? wu : 0.0);
+  }
+}
+
+// fraction to the boundary for one primal entry (ipm.py:265-273)
+__device__ __forceinline__ double ftb1(double val, double dv, double lo, double hi, double tau) {
+  double a = 1.0;
+  if (dv < 0 && isfinite(lo)) a = fmin(a, -tau * (val - lo) / dv);
+  if (dv > 0 && isfinite(hi)) a = fmin(a, tau * (hi - val) / dv);
+  return a;
+}
+__device__ __forceinline__ double dftb1(double z, double dz, double tau) {
+  return dz < 0 ? -tau * z / dz : 1.0;
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+direction_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double mu, double tau, RedSpec rs) {
+  double acc[4] = {1.0, 1.0, 1.0, 0.0};
+  const int64_t len = n > m ? n : m;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+    if (i < n) {
+      acc[0] = fmin(acc[0], ftb1(v.x[i], st.x[i], v.xl[i], v.xu[i], tau));
+      acc[2] = fmin(acc[2], fmin(dftb1(v.zxl[i], st.zxl[i], tau), dftb1(v.zxu[i], st.zxu[i], tau)));
+      double g = v.grad[i];
+      if (isfinite(v.dxl[i])) g -= mu / v.dxl[i];
+      if (isfinite(v.dxu[i])) g += mu / v.dxu[i];
+      acc[3] += g * st.x[i];
+    }
+    if (i < m) {
+      acc[1] = fmin(acc[1], ftb1(v.s[i], st.s[i], v.sl[i], v.su[i], tau));
+      acc[2] = fmin(acc[2], fmin(dftb1(v.zsl[i], st.zsl[i], tau), dftb1(v.zsu[i], st.zsu[i], tau)));
+      double g = 0.0;
+      if (isfinite(v.dsl[i])) g -= mu / v.dsl[i];
+      if (isfinite(v.dsu[i])) g += mu / v.dsu[i];
+      acc[3] += g * st.s[i];
+    }
+  }
+  grid_reduce(rs, acc);
+}
+
+__global__ void trial_point_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double alpha,
+                                   double *xt, double *s_t) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) xt[i] = v.x[i] + alpha * st.x[i];
+  if (i < m) s_t[i] = v.s[i] + alpha * st.s[i];
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+trial_merit_kernel(int64_t n, int64_t m, gn_ipm_vecs v, const double *ct, const double *xt,
+                   const double *s_t, RedSpec rs) {
+  double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t len = n > m ? n : m;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < len;
+       i += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+    if (i < n) {
+      const double x = xt[i];
+      if (isfinite(v.xl[i])) acc[1] += log(x - v.xl[i]);
+      if (isfinite(v.xu[i])) acc[2] += log(v.xu[i] - x);
+    }
+    if (i < m) {
+      const double s = s_t[i];
+      acc[0] += fabs(ct[i] - s);
+      if (isfinite(v.sl[i])) acc[3] += log(s - v.sl[i]);
+      if (isfinite(v.su[i])) acc[4] += log(v.su[i] - s);
+    }
+  }
+  grid_reduce(rs, acc);
+}
+
+__device__ __forceinline__ double safeguard(double z, double w, double mu, double ks) {
+  if (!isfinite(w)) return z;
+  return fmin(fmax(z, mu / (ks * w)), ks * mu / w);
+}
+
+__global__ void accept_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double alpha, double az,
+                              double mu, double ks, int32_t *flags) {
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double x = v.x[i] + alpha * st.x[i];
+    v.x[i] = x;
+    const double wl = width_lo(x, v.xl[i]), wu = width_hi(x, v.xu[i]);
+    v.zxl[i] = safeguard(v.zxl[i] + az * st.zxl[i], wl, mu, ks);
+    v.zxu[i] = safeguard(v.zxu[i] + az * st.zxu[i], wu, mu, ks);
+    if ((isfinite(wl) && !(wl > 0.0)) || (isfinite(wu) && !(wu > 0.0))) atomicOr(flags, 2);
+  }
+  if (i < m) {
+    const double s = v.s[i] + alpha * st.s[i];
+    v.s[i] = s;
+    v.y[i] = v.y[i] + alpha * st.y[i];
+    const double wl = width_lo(s, v.sl[i]), wu = width_hi(s, v.su[i]);
+    v.zsl[i] = safeguard(v.zsl[i] + az * st.zsl[i], wl, mu, ks);
+    v.zsu[i] = safeguard(v.zsu[i] + az * st.zsu[i], wu, mu, ks);
+    if ((isfinite(wl) && !(wl > 0.0)) || (isfinite(wu) && !(wu > 0.0))) atomicOr(flags, 4);
+  }
+}
+
+unsigned ew_blocks(int64_t len) { return static_cast<unsigned>(len > 0 ? (len + 255) / 256 : 1); }
+
+}  // namespace
+}  // namespace gn
+
+using namespace gn;
+#define ST(s) static_cast<cudaStream_t>(s)
+
+extern "C" int gn_ipm_prep(gn_kkt *K, const gn_ipm_vecs *v, int32_t n_mu, const double *mus_host,
+                           double *scal, void *stream) {
+  return guarded([&] {
+    GN_REQUIRE(n_mu >= 0 && n_mu <= GN_IPM_MAX_MU, "too many barrier candidates");
+    MuList mus{};
+    mus.n = n_mu;
+    for (int k = 0; k < n_mu; ++k) mus.mu[k] = mus_host[k];
+    int ops_x[4 + GN_IPM_MAX_MU] = {RED_MAX, RED_SUM, RED_SUM, RED_SUM};
+    for (int k = 0; k < n_mu; ++k) ops_x[4 + k] = RED_MAX;
+    int ops_s[7 + GN_IPM_MAX_MU] = {RED_MAX, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    for (int k = 0; k < n_mu; ++k) ops_s[7 + k] = RED_MAX;
+    GN_CUDA(cudaMemsetAsync(scal, 0, sizeof(double) * GN_PREP_DOUBLES, ST(stream)));
+    if (K->n)
+      prep_x_kernel<<<red_grid(K->n), kRedThreads, 0, ST(stream)>>>(
+          K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *v, mus, spec(*K, scal, 4 + n_mu, ops_x));
+    if (K->m)
+      prep_s_kernel<<<red_grid(K->m), kRedThreads, 0, ST(stream)>>>(K->m, *v, mus,
+                                                                  spec(*K, scal + GN_PREP_S, 7 + n_mu, ops_s));
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_pvec(gn_kkt *K, const gn_ipm_vecs *v, double mu, gn_vec7 *pv, void *stream) {
+  return guarded([&] {
+    pvec_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, mu, *pv);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_direction(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double mu, double tau,
+                                double *scal, void *stream) {
+  return guarded([&] {
+    int ops[4] = {RED_MIN, RED_MIN, RED_MIN, RED_SUM};
+    direction_kernel<<<red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream)>>>(
+        K->n, K->m, *v, *steps, mu, tau, spec(*K, scal, 4, ops));
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_trial_point(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
+                                  double *xt, double *st, void *stream) {
+  return guarded([&] {
+    trial_point_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, *steps, alpha,
+                                                                               xt, st);
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_trial_merit(gn_kkt *K, const gn_ipm_vecs *v, const double *ct, const double *xt,
+                                  const double *st, double *scal, void *stream) {
+  return guarded([&] {
+    int ops[5] = {RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    trial_merit_kernel<<<red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream)>>>(
+        K->n, K->m, *v, ct, xt, st, spec(*K, scal, 5, ops));
+    GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_accept(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
+                             double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream) {
+  return guarded([&] {
+    accept_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, *steps, alpha,
+                                                                          alpha_z, mu, kappa_sigma, flags);
+    GN_LAUNCH_CHECK();
+  });
+}

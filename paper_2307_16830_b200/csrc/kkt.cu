@@ -12,36 +12,13 @@
 
 namespace gn {
 
-struct Kkt {
-  int64_t n = 0, m = 0, nh = 0, nj = 0, nk = 0;
-  bool has_assembly = false;
-  struct Dev {
-    int64_t *a_rowptr = nullptr;   // A by rows (jac order)
-    int32_t *a_col = nullptr;
-    int64_t *at_ptr = nullptr;     // A by columns: jac positions + rows
-    int32_t *at_p = nullptr, *at_row = nullptr;
-    int64_t *w_ptr = nullptr;      // symmetric W per row: hess positions + partner
-    int32_t *w_p = nullptr, *w_j = nullptr;
-    int64_t *k_ptr = nullptr;      // assembly: per K slot products (row, s1, s2)
-    int32_t *k_row = nullptr, *k_s1 = nullptr, *k_s2 = nullptr;
-    int32_t *k_w = nullptr, *k_diag = nullptr;
-    double *partials = nullptr;
-    unsigned int *counter = nullptr;
-    double *scratch = nullptr;     // m doubles
-  } d;
-  ~Kkt() {
-    void *ps[] = {d.a_rowptr, d.a_col, d.at_ptr, d.at_p, d.at_row, d.w_ptr, d.w_p, d.w_j,
-                  d.k_ptr, d.k_row, d.k_s1, d.k_s2, d.k_w, d.k_diag, d.partials, d.counter,
-                  d.scratch};
-    for (void *p : ps) dev_free(p);
-  }
-};
+Kkt::~Kkt() {
+  void *ps[] = {d.a_rowptr, d.a_col, d.at_ptr, d.at_p, d.at_row, d.w_ptr, d.w_p, d.w_j,
+                d.k_ptr, d.k_row, d.k_s1, d.k_s2, d.k_w, d.k_diag, d.partials, d.counter,
+                d.scratch};
+  for (void *p : ps) dev_free(p);
+}
 
-}  // namespace gn
-
-struct gn_kkt : gn::Kkt {};
-
-namespace gn {
 namespace {
 
 constexpr int kT = 256;
@@ -86,7 +63,7 @@ __device__ __forceinline__ double dd_round(dd x) { return x.hi + x.lo; }
 __global__ void sigma_kernel(int64_t len, const double *dl, const double *du, const double *zl,
                              const double *zu, double *out) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
-  if (i < len) out[i] = zl[i] * inv_or_zero(dl[i]) + zu[i] * inv_or_zero(du[i]);
+  if (i < len) out[i] = __dadd_rn(__dmul_rn(zl[i], inv_or_zero(dl[i])), __dmul_rn(zu[i], inv_or_zero(du[i])));
 }
 
 // W v from the lower triangle: first every entry's row contribution, then

@@ -13,10 +13,10 @@ enum RedOp : int { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
 
 constexpr int kRedThreads = 256;
 constexpr int kRedMaxBlocks = 296;   // 2 CTAs per SM on 148 SMs
-constexpr int kRedMaxSlots = 24;
+constexpr int kRedMaxSlots = 40;
 
 struct RedSpec {
-  int k;                      // number of reduced quantities
+  int k;                      // number of reduced quantities (<= kRedMaxSlots)
   int op[kRedMaxSlots];       // RedOp per slot
   double *out;                // k outputs (device)
   double *partials;           // kRedMaxBlocks * kRedMaxSlots scratch
@@ -42,8 +42,9 @@ inline int red_grid(int64_t n, int per_thread = 1) {
   return static_cast<int>(g);
 }
 
-// Reduce `vals[0..K)` held by every thread of the grid; thread 0 of the last
-// CTA writes spec.out.  Must be called by all threads of every CTA.
+// Reduce vals[0..spec.k) held by every thread of the grid (blockDim ==
+// kRedThreads); thread 0 of the last CTA writes spec.out.  Must be reached
+// by all threads of every CTA.
 template <int K>
 __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
   __shared__ double sh[K][kRedThreads / 32];
@@ -51,14 +52,14 @@ __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
+    if (k >= spec.k) break;
     double v = vals[k];
     for (int o = 16; o > 0; o >>= 1) v = red_combine(spec.op[k], v, __shfl_down_sync(0xffffffffu, v, o));
     if (lane == 0) sh[k][warp] = v;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < spec.k; ++k) {
       double v = sh[k][0];
       for (int w = 1; w < nw; ++w) v = red_combine(spec.op[k], v, sh[k][w]);
       spec.partials[blockIdx.x * kRedMaxSlots + k] = v;
@@ -70,10 +71,10 @@ __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < spec.k; ++k) {
       double v = __ldcg(spec.partials + k);
-      for (unsigned b = 1; b < gridDim.x; ++b) v = red_combine(spec.op[k], v, __ldcg(spec.partials + b * kRedMaxSlots + k));
+      for (unsigned b = 1; b < gridDim.x; ++b)
+        v = red_combine(spec.op[k], v, __ldcg(spec.partials + b * kRedMaxSlots + k));
       spec.out[k] = v;
     }
     *spec.counter = 0u;

@@ -1,0 +1,487 @@
+"""Condensed-space interior-point loop with every iterate resident in HBM.
+
+Same algorithm, options, statuses and report as reference
+src/gridnlp/ipm.py (Algorithm 1): equality relaxation, frozen
+gradient scaling, the kappa_eps barrier update, the condensed Newton step
+with double-double refinement, fraction-to-boundary, the filter / Armijo
+line search and the kappa_sigma dual safeguard.
+
+The driver stays in Python and only sequences device work: AD kernels
+(csrc/ad.cu), fused iterate/merit reductions (csrc/ipm.cu), condensed
+assembly and recoveries (csrc/kkt.cu) and the multifrontal factor/solve
+(csrc/chol.cu).  Host <-> device traffic per iteration is a handful of
+scalar blocks at the points where the reference's control flow branches
+(residual norms, PD flag, refinement norms, step lengths, trial merits).
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import device as D
+from .autodiff import C, F, GRAD, HESS, JAC, NonFiniteResult, evaluator
+from .kkt import (CondensedBackend, DegenerateInterior, KKTWorkspace, PVec, RegState,
+                  RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
+                  solve_with_regularization)
+
+OPTIMAL = "optimal"
+MAX_ITER = "max_iter"
+REGULARIZATION_EXHAUSTED = "regularization_exhausted"
+LINE_SEARCH_FAILURE = "line_search_failure"
+EVAL_ERROR = "eval_error"
+
+
+@dataclass
+class SolverOptions:
+    """Options and defaults of the reference (ipm.py:43-74)."""
+    tol: float = 1e-4
+    max_iter: int = 3000
+    mu_init: float = 0.1
+    bound_push: float = 0.01
+    bound_relax: float | None = None
+    mu_min: float | None = None
+    kappa_eps: float = 10.0
+    kappa_mu: float = 0.2
+    theta_mu: float = 1.5
+    tau_min: float = 0.99
+    eta_phi: float = 1e-8
+    gamma_theta: float = 1e-5
+    gamma_phi: float = 1e-5
+    s_theta: float = 1.1
+    s_phi: float = 2.3
+    delta: float = 1.0
+    kappa_sigma: float = 1e10
+    alpha_min: float = 1e-12
+    s_max: float = 100.0
+    fixed_var_eps: float = 1e-8
+    scaling: bool = True
+    backend: str = "condensed"
+    log_level: int = 0
+    record_trace: bool = True
+    keep_workspace: bool = False
+    ordering: object = None   # optional injected fill-reducing permutation
+
+    def __post_init__(self):
+        if self.tol <= 0.0:
+            raise ValueError("tol must be positive")
+        if self.backend != "condensed":
+            raise ValueError("only the condensed GPU backend is provided "
+                             "(the dense augmented LDL^T is the CPU oracle's)")
+
+
+@dataclass
+class SolveReport:
+    status: str
+    objective: float = np.nan
+    constraint_violation: float = np.nan
+    residual_scaled: float = np.nan
+    iterations: int = 0
+    seconds: dict = field(default_factory=dict)
+    final_mu: float = np.nan
+    n_var: int = 0
+    n_con: int = 0
+    refinement_relative_residual: float = np.nan
+    message: str = ""
+    x: np.ndarray | None = None
+    trace: list = field(default_factory=list)
+    debug: dict = field(default_factory=dict)
+
+    @property
+    def success(self) -> bool:
+        return self.status == OPTIMAL
+
+
+# -- host helpers (once per solve; identical to the reference) -------------
+def relax_equalities(m, ranges, tol):
+    """Slack intervals (ipm.py:112-123)."""
+    if ranges is None:
+        lo, hi = np.zeros(m), np.zeros(m)
+    else:
+        r = np.asarray(ranges, dtype=float)
+        lo, hi = r[:, 0].copy(), r[:, 1].copy()
+    with np.errstate(invalid="ignore"):
+        sl = np.where(np.isfinite(lo), lo - tol * np.maximum(1.0, np.abs(lo)), -np.inf)
+        su = np.where(np.isfinite(hi), hi + tol * np.maximum(1.0, np.abs(hi)), np.inf)
+    return sl, su
+
+
+def initial_slacks(g0, sl, su, tol, push):
+    """Clamp g(x0) into the strict interior (ipm.py:126-134)."""
+    lo = np.where(np.isfinite(sl), sl + push * tol, -np.inf)
+    hi = np.where(np.isfinite(su), su - push * tol, np.inf)
+    s = np.minimum(np.maximum(g0, lo), hi)
+    crossed = lo > hi
+    return np.where(crossed, 0.5 * (sl + su), s) if np.any(crossed) else s
+
+
+def kkt_residual(dual_x, dual_s, primal, comps, z_l1, y_l1, m, n_bounds, s_max=100.0):
+    """Scaled optimality residual (ipm.py:150-157) from arrays."""
+    amax = lambda *arrs: max([0.0] + [float(np.abs(a).max()) for a in arrs if np.size(a)])
+    return kkt_residual_scalars(max(amax(dual_x), amax(dual_s)), amax(primal), amax(*comps),
+                                z_l1, y_l1, m, n_bounds, s_max)
+
+
+def kkt_residual_scalars(dual_max, primal_max, comp_max, z_l1, y_l1, m, n_bounds, s_max=100.0):
+    """Same residual from the device reductions."""
+    s_d = max(s_max, (y_l1 + z_l1) / max(1, m + n_bounds)) / s_max
+    s_c = max(s_max, z_l1 / max(1, n_bounds)) / s_max
+    comp = comp_max / s_c if n_bounds else 0.0
+    return max(dual_max / s_d, primal_max, comp)
+
+
+class _Filter:
+    def __init__(self):
+        self.entries: list[tuple[float, float]] = []
+
+    def acceptable(self, theta, phi):
+        return all(theta < th or phi < ph for th, ph in self.entries)
+
+    def add(self, theta, phi):
+        self.entries = [(th, ph) for th, ph in self.entries if not (th >= theta and ph >= phi)]
+        self.entries.append((theta, phi))
+
+    def clear(self):
+        self.entries.clear()
+
+
+def _mu_candidates(mu, mu_min, opts, k):
+    """[0, mu, update(mu), ...] -- the values the barrier loop may visit."""
+    out = [0.0, mu]
+    cur = mu
+    while len(out) < k and cur > mu_min * (1 + 1e-12):
+        cur = max(mu_min, min(opts.kappa_mu * cur, cur ** opts.theta_mu))
+        out.append(cur)
+    return out
+
+
+class _Timer:
+    """CUDA-event phase timing (replaces the reference's perf_counter splits)."""
+
+    def __init__(self):
+        self.spans = {"ad": [], "linear": []}
+
+    def start(self):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def stop(self, name, ev0):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.spans[name].append((ev0, e))
+
+    def totals(self):
+        return {k: sum(a.elapsed_time(b) for a, b in v) / 1e3 for k, v in self.spans.items()}
+
+
+class _DeviceSolve:
+    """Device buffers and scalar mailboxes of one solve."""
+
+    def __init__(self, model, opts, ranges):
+        self.model = model
+        self.opts = opts
+        n, m = model.n_var, model.n_con
+        self.n, self.m = n, m
+        self.tol_r = opts.bound_relax if opts.bound_relax is not None else opts.tol
+        xl, xu = model.lower.copy(), model.upper.copy()
+        fixed = xl == xu
+        if np.any(fixed):
+            eps = opts.fixed_var_eps * np.maximum(1.0, np.abs(xl))
+            xl, xu = np.where(fixed, xl - eps, xl), np.where(fixed, xu + eps, xu)
+        self.xl_h, self.xu_h = xl, xu
+        self.x0 = np.minimum(np.maximum(model.start, xl), xu)
+        self.ev = evaluator(model)
+        dev = D.require_cuda()
+        self.dev = dev
+        # frozen gradient scaling at x0 (ipm.py:179-193)
+        x0d = D.to_dev(self.x0)
+        g0 = D.empty(n)
+        j0 = D.empty(max(1, model.nnz_jac))
+        self.ev.flags.zero_()
+        self.ev.launch(x0d, GRAD | JAC, grad=g0, jac=j0)
+        fl = int(self.ev.flags.item())
+        self.ev.raise_on_flags(fl)
+        g0h, j0h = D.to_host(g0), D.to_host(j0)[:model.nnz_jac]
+        if opts.scaling:
+            gm = float(np.abs(g0h).max()) if n else 0.0
+            self.obj_scale = min(1.0, 100.0 / gm) if gm > 0 else 1.0
+            rmax = np.zeros(m)
+            if j0h.size:
+                np.maximum.at(rmax, model.jac_rows, np.abs(j0h))
+            self.con_scale_h = np.ones(m)
+            pos = rmax > 0
+            self.con_scale_h[pos] = np.minimum(1.0, 100.0 / rmax[pos])
+        else:
+            self.obj_scale, self.con_scale_h = 1.0, np.ones(m)
+        if ranges is None:
+            self.rlo, self.rhi = np.zeros(m), np.zeros(m)
+        else:
+            r = np.asarray(ranges, dtype=float)
+            self.rlo, self.rhi = r[:, 0].copy(), r[:, 1].copy()
+        scaled = np.column_stack([self.rlo * self.con_scale_h, self.rhi * self.con_scale_h]) if m else None
+        self.sl_h, self.su_h = relax_equalities(m, scaled, self.tol_r)
+        self.n_bounds = int(np.isfinite(xl).sum() + np.isfinite(xu).sum()
+                            + np.isfinite(self.sl_h).sum() + np.isfinite(self.su_h).sum())
+        # device state
+        td = lambda a: D.to_dev(a)
+        self.xl, self.xu, self.sl, self.su = td(xl), td(xu), td(self.sl_h), td(self.su_h)
+        self.con_scale = td(self.con_scale_h) if m else D.zeros(1)
+        self.x = x0d.clone()
+        self.s, self.y = D.zeros(m), D.zeros(m)
+        self.zxl = td(np.where(np.isfinite(xl), 1.0, 0.0))
+        self.zxu = td(np.where(np.isfinite(xu), 1.0, 0.0))
+        self.zsl = td(np.where(np.isfinite(self.sl_h), 1.0, 0.0))
+        self.zsu = td(np.where(np.isfinite(self.su_h), 1.0, 0.0))
+        self.grad, self.c = D.empty(n), D.empty(max(1, m))
+        self.dual_x, self.dual_s, self.primal = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
+        self.xt, self.st, self.ct = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
+        # scalar mailbox: [0:48) prep | 48 f | 49 f_trial | 50.. misc
+        self.scal = D.zeros(96)
+        self.host = torch.zeros(96, dtype=torch.float64, pin_memory=True)
+        self.host_flags = torch.zeros(2, dtype=torch.int32, pin_memory=True)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)   # [AD flags, IPM flags]
+
+    def vecs(self, ws) -> L.IpmVecs:
+        return L.IpmVecs(*(t.data_ptr() for t in (
+            self.x, self.s, self.y, self.zxl, self.zxu, self.zsl, self.zsu, self.xl, self.xu,
+            self.sl, self.su, ws.dxl, ws.dxu, ws.dsl, ws.dsu, ws.sigma_x, ws.sigma_s, self.grad,
+            self.c, ws.a_vals, self.dual_x, self.dual_s, self.primal)))
+
+    def read(self, lo, hi):
+        """Copy scal[lo:hi] and both flag words to the host (one stream sync)."""
+        self.host[lo:hi].copy_(self.scal[lo:hi], non_blocking=True)
+        self.host_flags.copy_(self.flags, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return self.host[lo:hi].numpy(), int(self.host_flags[0]), int(self.host_flags[1])
+
+
+def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -> SolveReport:
+    """Solve min f s.t. g in ranges, bounds -- on the GPU (ipm.py:301-563)."""
+    opts = options if options is not None else SolverOptions()
+    t_start = time.perf_counter()
+    report = SolveReport(status=MAX_ITER, n_var=model.n_var, n_con=model.n_con)
+    try:
+        P = _DeviceSolve(model, opts, constraint_ranges)
+    except NonFiniteResult as exc:
+        report.status = EVAL_ERROR
+        report.message = str(exc)
+        report.seconds = {"total": time.perf_counter() - t_start, "ad": 0.0, "linear": 0.0,
+                          "internal": 0.0}
+        return report
+    n, m = P.n, P.m
+    mu_min = opts.mu_min if opts.mu_min is not None else opts.tol / 10.0
+    lib = L.lib()
+    stream = D.stream_ptr()
+    timer = _Timer()
+
+    ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols)
+    # the workspace reads the solver's duals in place (no copies per iteration)
+    ws.zxl, ws.zxu, ws.zsl, ws.zsu = P.zxl, P.zxu, P.zsl, P.zsu
+    backend = CondensedBackend(ws, ordering=opts.ordering)
+    reg = RegState()
+    V = P.vecs(ws)
+    ev = P.ev
+    fil = _Filter()
+    state = {"mu": opts.mu_init, "it": 0}
+    flagp = L.ptr(P.flags)
+
+    def finish(status, message=""):
+        torch.cuda.current_stream().synchronize()
+        total = time.perf_counter() - t_start
+        report.status = status
+        report.message = message
+        report.iterations = state["it"]
+        report.final_mu = state["mu"]
+        report.x = D.to_host(P.x)
+        try:
+            from .autodiff import eval_constraints, eval_objective
+
+            report.objective = eval_objective(model, P.x)
+            g = D.to_host(eval_constraints(model, P.x)) if m else np.zeros(0)
+            report.constraint_violation = (float(np.maximum(np.maximum(P.rlo - g, 0.0),
+                                                            np.maximum(g - P.rhi, 0.0)).max())
+                                           if m else 0.0)
+        except NonFiniteResult:
+            pass
+        sec = timer.totals()
+        internal = max(0.0, total - sec["ad"] - sec["linear"])
+        report.seconds = {"total": total, "ad": sec["ad"], "linear": sec["linear"],
+                          "internal": internal}
+        if opts.record_trace:
+            report.debug["filter"] = list(fil.entries)
+        report.debug["n_factorizations"] = backend.n_factorizations
+        report.debug["symbolic"] = dict(backend.symbolic.info)
+        if opts.keep_workspace:
+            report.debug["workspace"] = ws
+            report.debug["backend"] = backend
+            report.debug["problem"] = P
+        return report
+
+    def check_ipm_flags(ipm_flags):
+        if ipm_flags & 2:
+            raise DegenerateInterior("x slack lost strict interiority")
+        if ipm_flags & 4:
+            raise DegenerateInterior("s slack lost strict interiority")
+
+    # initial slacks from g(x0) (ipm.py:371-380)
+    P.flags.zero_()
+    ev.flags.zero_()
+    t0 = timer.start()
+    ev.launch(P.x, C, con_scale=P.con_scale, c=P.c)
+    timer.stop("ad", t0)
+    torch.cuda.current_stream().synchronize()
+    if int(ev.flags.item()):
+        return finish(EVAL_ERROR, "constraint evaluation produced a non-finite value")
+    g0 = D.to_host(P.c)[:m]
+    s0 = initial_slacks(g0, P.sl_h, P.su_h, P.tol_r, opts.bound_push)
+    P.s.copy_(D.to_dev(s0)) if m else None
+    theta0 = float(np.abs(g0 - s0).sum()) if m else 0.0
+    theta_min = 1e-4 * max(1.0, theta0)
+    theta_max = 1e4 * max(1.0, theta0)
+    f_ptr = L.ptr(P.scal[48:49])
+    ft_ptr = L.ptr(P.scal[49:50])
+    ev_flags = ev.flags
+
+    for _ in range(opts.max_iter):
+        mu = state["mu"]
+        # ---- derivatives at x (ipm.py:384-391)
+        ev_flags.zero_()
+        t0 = timer.start()
+        ev.launch(P.x, F | C | GRAD | JAC | HESS, y=P.y, obj_weight=P.obj_scale,
+                  con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
+                  grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
+        timer.stop("ad", t0)
+        # ---- widths, Sigma, residual blocks and reductions (ipm.py:393-429)
+        cands = _mu_candidates(mu, mu_min, opts, L.IPM_MAX_MU)
+        mus = (ctypes.c_double * len(cands))(*cands)
+        L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal), stream))
+        P.flags[0:1].copy_(ev_flags)
+        sc, adf, ipf = P.read(0, 49)
+        check_ipm_flags(ipf)
+        if adf:
+            try:
+                ev.raise_on_flags(adf)
+            except NonFiniteResult as exc:
+                return finish(EVAL_ERROR, str(exc))
+        fval = float(sc[48])
+        S0 = L.PREP_S
+        dual_max = max(sc[0], sc[S0 + 0])
+        primal_max = sc[S0 + 1]
+        z_l1 = sc[1] + sc[S0 + 2]
+        y_l1 = sc[S0 + 3]
+        comp = lambda k: max(sc[4 + k] if n else 0.0, sc[S0 + 7 + k] if m else 0.0)
+        resid = lambda k: kkt_residual_scalars(dual_max, primal_max, comp(k), z_l1, y_l1, m,
+                                               P.n_bounds, opts.s_max)
+        e_0 = resid(0)
+        if e_0 < opts.tol:
+            report.residual_scaled = e_0
+            return finish(OPTIMAL)
+        k = 1
+        e_mu = resid(k)
+        while e_mu <= opts.kappa_eps * mu and mu > mu_min * (1 + 1e-12):
+            mu = max(mu_min, min(opts.kappa_mu * mu, mu ** opts.theta_mu))
+            fil.clear()
+            k += 1
+            if k < len(cands) and cands[k] == mu:
+                e_mu = resid(k)
+            else:   # beyond the precomputed candidates: one more reduction pass
+                more = (ctypes.c_double * 2)(0.0, mu)
+                L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), 2, more, L.ptr(P.scal), stream))
+                sc2, _, _ = P.read(0, 48)
+                sc = np.concatenate([sc2, sc[48:]])
+                cands = [0.0, mu]
+                k = 1
+                e_mu = resid(1)
+        state["mu"] = mu
+        theta_cur = float(sc[S0 + 4]) if m else 0.0
+        phi_cur = fval
+        for lsum in (sc[2], sc[3], sc[S0 + 5], sc[S0 + 6]):
+            phi_cur -= mu * float(lsum)
+        # ---- Newton step (ipm.py:434-453)
+        pv = PVec.empty(n, m)
+        pvc = pv.c_struct()
+        L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), stream))
+        t0 = timer.start()
+        try:
+            (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg)
+            steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
+            ir = iterative_refinement(ws, backend, steps, pv)
+        except RegularizationExhausted as exc:
+            timer.stop("linear", t0)
+            return finish(REGULARIZATION_EXHAUSTED, str(exc))
+        timer.stop("linear", t0)
+        report.refinement_relative_residual = ir.relative_residual
+        # ---- fraction to the boundary and dphi (ipm.py:455-476)
+        tau = max(opts.tau_min, 1.0 - mu)
+        stc = steps.c_struct()
+        L.check(lib.gn_ipm_direction(ws.handle, ctypes.byref(V), ctypes.byref(stc), mu, tau,
+                                     L.ptr(P.scal[50:54]), stream))
+        d, _, _ = P.read(50, 54)
+        alpha_max = min(float(d[0]), float(d[1]))
+        alpha_z, dphi = float(d[2]), float(d[3])
+        # ---- filter line search (ipm.py:478-519)
+        alpha = alpha_max
+        accepted = f_type = False
+        theta_t = phi_t = np.nan
+        while alpha >= opts.alpha_min:
+            L.check(lib.gn_ipm_trial_point(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha,
+                                           L.ptr(P.xt), L.ptr(P.st), stream))
+            ev_flags.zero_()
+            t0 = timer.start()
+            ev.launch(P.xt, F | C, con_scale=P.con_scale, obj_scale=P.obj_scale,
+                      f=P.scal[49:50], c=P.ct)
+            timer.stop("ad", t0)
+            L.check(lib.gn_ipm_trial_merit(ws.handle, ctypes.byref(V), L.ptr(P.ct), L.ptr(P.xt),
+                                           L.ptr(P.st), L.ptr(P.scal[54:59]), stream))
+            P.flags[0:1].copy_(ev_flags)
+            tv, adf, _ = P.read(49, 59)
+            if adf:
+                alpha *= 0.5
+                continue
+            ft = float(tv[0])
+            theta_t = float(tv[5]) if m else 0.0
+            phi_t = ft
+            for lsum in tv[6:10]:
+                phi_t -= mu * float(lsum)
+            if not np.isfinite(phi_t) or theta_t > theta_max:
+                alpha *= 0.5
+                continue
+            if not fil.acceptable(theta_t, phi_t):
+                alpha *= 0.5
+                continue
+            switching = (dphi < 0.0 and alpha * (-dphi) ** opts.s_phi
+                         > opts.delta * theta_cur ** opts.s_theta)
+            if theta_cur <= theta_min and switching:
+                if phi_t <= phi_cur + opts.eta_phi * alpha * dphi:
+                    accepted = f_type = True
+                    break
+            elif (theta_t <= (1.0 - opts.gamma_theta) * theta_cur
+                  or phi_t <= phi_cur - opts.gamma_phi * theta_cur):
+                accepted = True
+                break
+            alpha *= 0.5
+        if not accepted:
+            return finish(LINE_SEARCH_FAILURE, f"step size below {opts.alpha_min:g}")
+        if not f_type:
+            fil.add((1.0 - opts.gamma_theta) * theta_cur, phi_cur - opts.gamma_phi * theta_cur)
+        # ---- accept + dual safeguard + interiority (ipm.py:521-548)
+        L.check(lib.gn_ipm_accept(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha, alpha_z,
+                                  mu, opts.kappa_sigma, L.ptr(P.flags[1:2]), stream))
+        state["it"] += 1
+        if opts.record_trace:
+            report.trace.append((state["it"], fval / P.obj_scale, float(primal_max),
+                                 float(dual_max), mu, alpha, delta_w))
+            report.debug.setdefault("accepted", []).append((theta_t, phi_t, list(fil.entries)))
+            report.debug.setdefault("ir_rounds", []).append(ir.rounds)
+        if opts.log_level >= 2:
+            print(f"iter {state['it']:4d} obj {fval / P.obj_scale: .8e} inf_pr {primal_max:.2e} "
+                  f"inf_du {dual_max:.2e} mu {mu:.1e} alpha {alpha:.2e} dw {delta_w:.1e}")
+        report.residual_scaled = e_0
+    torch.cuda.current_stream().synchronize()
+    check_ipm_flags(int(P.flags[1].item()))
+    return finish(MAX_ITER)

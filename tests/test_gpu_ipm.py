@@ -1,0 +1,87 @@
+"""Interior-point behaviour on small problems (GPU), after test_ipm_core.py:103-200."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2307_16830_b200 import SolverOptions, solve  # noqa: E402
+from paper_2307_16830_b200.expressions import log, param, var  # noqa: E402
+from paper_2307_16830_b200.ipm import EVAL_ERROR, LINE_SEARCH_FAILURE, MAX_ITER, OPTIMAL  # noqa: E402
+from paper_2307_16830_b200.model import ModelBuilder  # noqa: E402
+
+
+def box(n, lo=-50.0, hi=50.0, start=0.0):
+    b = ModelBuilder()
+    b.add_variables(n, np.full(n, lo), np.full(n, hi), np.full(n, start))
+    return b
+
+
+def quadratic_model(n=4):
+    b = box(n)
+    b.add_objective((var(0) - param(0)) ** 2, np.arange(n).reshape(-1, 1),
+                    np.arange(n, dtype=float).reshape(-1, 1))
+    return b.finalize()
+
+
+def eq_model():
+    b = box(2, -10, 10, 0.5)
+    b.add_objective(var(0) ** 2, np.array([[0], [1]]), np.zeros((2, 0)))
+    b.add_constraints(var(0) + var(1) - 2.0, np.array([[0, 1]]), np.zeros((1, 0)))
+    return b.finalize()
+
+
+def test_unconstrained_quadratic():
+    rep = solve(quadratic_model(), SolverOptions(tol=1e-6))
+    assert rep.status == OPTIMAL and rep.iterations <= 15
+    np.testing.assert_allclose(rep.x, np.arange(4.0), atol=1e-4)
+
+
+def test_equality_constrained():
+    rep = solve(eq_model(), SolverOptions(tol=1e-6))
+    assert rep.status == OPTIMAL
+    np.testing.assert_allclose(rep.x, [1.0, 1.0], atol=1e-4)
+
+
+def test_infeasible_not_optimal():
+    b = box(1, -5, 5, 0.4)
+    b.add_constraints(var(0), np.array([[0]]), np.zeros((1, 0)))
+    b.add_constraints(var(0) - 1.0, np.array([[0]]), np.zeros((1, 0)))
+    rep = solve(b.finalize(), SolverOptions(tol=1e-4, max_iter=150))
+    assert rep.status in (LINE_SEARCH_FAILURE, MAX_ITER)
+
+
+def test_active_bound_and_range():
+    b = box(1, -5.0, 1.0)
+    b.add_objective((var(0) - 3.0) ** 2, np.array([[0]]), np.zeros((1, 0)))
+    rep = solve(b.finalize(), SolverOptions(tol=1e-6))
+    assert rep.status == OPTIMAL and rep.x[0] == pytest.approx(1.0, abs=1e-4)
+    b = box(1, -20.0, 20.0)
+    b.add_objective((var(0) - 5.0) ** 2, np.array([[0]]), np.zeros((1, 0)))
+    b.add_constraints(var(0), np.array([[0]]), np.zeros((1, 0)))
+    rep = solve(b.finalize(), SolverOptions(tol=1e-6), constraint_ranges=np.array([[-1.0, 2.0]]))
+    assert rep.status == OPTIMAL and rep.x[0] == pytest.approx(2.0, abs=1e-3)
+
+
+def test_eval_error_and_fixed_variable():
+    b = box(1, -5.0, 5.0, start=-2.0)
+    b.add_objective(log(var(0)), np.array([[0]]), np.zeros((1, 0)))
+    assert solve(b.finalize(), SolverOptions(tol=1e-6)).status == EVAL_ERROR
+    b = ModelBuilder()
+    b.add_variables(2, np.array([-5.0, 2.0]), np.array([5.0, 2.0]), np.array([0.0, 2.0]))
+    b.add_objective((var(0) - param(0)) ** 2, np.array([[0], [1]]), np.array([[1.0], [0.0]]))
+    rep = solve(b.finalize(), SolverOptions(tol=1e-6))
+    assert rep.status == OPTIMAL and rep.x[1] == pytest.approx(2.0, abs=1e-6)
+
+
+def test_invariants_determinism_mu_alpha_filter():
+    r1 = solve(eq_model(), SolverOptions(tol=1e-8))
+    r2 = solve(eq_model(), SolverOptions(tol=1e-8))
+    assert r1.trace == r2.trace and r1.objective == r2.objective
+    mus = [row[4] for row in r1.trace]
+    assert all(b <= a for a, b in zip(mus, mus[1:])) and min(mus) >= 1e-8 / 10.0
+    assert all(0.0 < row[5] <= 1.0 for row in r1.trace)
+    for theta, phi, entries in r1.debug.get("accepted", []):
+        for th, ph in entries[:-1]:
+            assert theta < th or phi < ph
+    sec = r1.seconds
+    assert sec["ad"] + sec["linear"] + sec["internal"] <= sec["total"] * 1.001
