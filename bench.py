@@ -1,0 +1,322 @@
+"""Benchmark: ACOPF solve time on B200 (BASELINE.json metric).
+
+Workload at N=1: C3 -- the 9,996-bus synthetic ACOPF (714 IEEE-14 tiles on a
+27-column mesh with angle/thermal limits), solved to
+tol 1e-6 (BASELINE.json configs[2], the headline end-to-end config).
+
+* a "step" = one complete interior-point solve from the reference start
+  point to tol 1e-6 (18 IPM iterations);
+* ``value``  = mean device time of a step with the model and its symbolic
+  plans resident in HBM (CUDA events on the solve stream; L2 flushed with a
+  512 MiB write between steps, outside the events);
+* ``e2e``    = the same solve through the public API ``solve(model, ...)``
+  from host arrays with no device state: plan uploads (H2D), symbolic
+  condensation, ordering, symbolic factorisation, the IPM and the D2H read
+  of x, wall-clock per step;
+* ``roofline`` for the dominant kernel (the multifrontal refactorisation,
+  chol.cu) = SURVEY.md §8(d) compulsory bytes (nnzK*12 + nnzL*12) / its
+  mean launch duration vs the measured HBM copy bandwidth;
+* ``cpu_baseline`` = the oracle port (oracle/, the reference algorithm
+  restated with the reference's own operation order) solving the same C3
+  instance on one host core with the ordering injected ("loop-fair",
+  BASELINE.md §3.4(b)).
+
+N > 1 (torchrun): a single ACOPF instance does not shard, so every rank
+solves its own replica ("replicas only") and rank 0 gathers the
+final x of every replica with one NCCL all_gather at the end of each step;
+time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+METRIC = "ACOPF solve time (s) + per-iter AD/condense/refactor ms, 10k–78k-bus grids"
+WORKLOADS = {"C3": 714, "C2": 143, "C4": 5606, "C1": 1}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _clock_sampler():
+    try:
+        return subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except Exception:
+        return None
+
+
+def _clock_summary(proc, gpu_index):
+    if proc is None:
+        return None
+    proc.terminate()
+    try:
+        out, _ = proc.communicate(timeout=5)
+    except Exception:
+        return None
+    sm, mx, reasons = [], None, set()
+    names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+    for line in out.strip().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 9 or f[0] != str(gpu_index):
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx = float(f[2])
+        except ValueError:
+            continue
+        for nm, v in zip(names, f[5:9]):
+            if v.lower() == "active":
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def build_model(workload, seed=None):
+    from paper_2307_16830_b200.acopf import build_acopf
+    from paper_2307_16830_b200.grids import tiled_case
+    from paper_2307_16830_b200.matpower import parse_matpower
+
+    return build_acopf(parse_matpower(tiled_case(WORKLOADS[workload], seed=seed)))
+
+
+def cpu_baseline(workload, tol, am=None):
+    """Oracle port of the reference on one host core, ordering injected."""
+    from oracle import ipm as OI
+    from oracle import model as OM
+    from paper_2307_16830_b200 import kkt, sparse
+
+    am = am or build_model(workload)
+    m = am.model
+    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
+    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
+    perm = sparse.amd_order(cs.matrix)   # bit-identical to amd_order; injected (loop-fair)
+    t = time.perf_counter()
+    rep = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol), am.ranges, ordering=perm)
+    dt = time.perf_counter() - t
+    return dt, rep
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port) on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import psutil  # noqa: F401  (available in the image)
+
+    am = build_model(args.workload)
+    warm = build_model("C1")
+    from oracle import ipm as OI
+    from oracle import model as OM
+
+    wm = warm.model
+    wom = OM.expand(wm.n_var, wm.n_con, OM.from_model(wm))
+    for _ in range(args.warmup):   # warm the code paths on the 14-bus tile
+        OI.solve(wom, wm.lower, wm.upper, wm.start, OI.Options(tol=args.tol), warm.ranges)
+    times, rep = [], None
+    budget = float(os.environ.get("REF_BUDGET_S", "240"))
+    t_all = time.perf_counter()
+    for k in range(args.steps):
+        dt, rep = cpu_baseline(args.workload, args.tol, am)
+        times.append(dt)
+        if time.perf_counter() - t_all > budget and k + 1 < args.steps:
+            break
+    v = float(np.mean(times))
+    cores = 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+        "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * v, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]} IEEE-14 tiles, limits, "
+                               f"tol {args.tol:g}", "n_var": am.model.n_var, "n_con": am.model.n_con},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"full {args.workload} solve to tol {args.tol:g} "
+                                   f"({rep.iterations} IPM iterations) per step, ordering injected "
+                                   "(loop-fair); warm-up on the 14-bus tile"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iterations": rep.iterations, "objective": rep.objective, "status": rep.status,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="C3", choices=tuple(WORKLOADS))
+    ap.add_argument("--tol", type=float, default=1e-6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_16830_b200 import SolverOptions, _lib, profiling, solve
+    from paper_2307_16830_b200 import device as D
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    am = build_model(args.workload)
+    model = am.model
+    opts = SolverOptions(tol=args.tol)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def one_solve():
+        rep = solve(model, opts, constraint_ranges=am.ranges)
+        if world > 1:   # final gather of every replica's solution (C1 in SURVEY §2.3)
+            x = torch.as_tensor(rep.x, device="cuda")
+            bufs = [torch.empty_like(x) for _ in range(world)]
+            dist.all_gather(bufs, x)
+        return rep
+
+    for _ in range(max(args.warmup, 1)):
+        rep = one_solve()
+    # ---- timed region: device-resident solves
+    _lib.stats(reset=True)
+    profiling.reset()
+    profiling.enable(True)
+    clocks = _clock_sampler() if rank == 0 else None
+    step_ms = []
+    barrier()
+    torch.cuda.synchronize()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = one_solve()
+        e1.record()
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    barrier()
+    torch.cuda.synchronize()
+    clk = _clock_summary(clocks, local) if rank == 0 else None
+    profiling.enable(False)
+    launches, _ = _lib.stats(reset=True)
+    phases = profiling.summary()
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total_ms.item()) / args.steps
+    iters = rep.iterations
+
+    # ---- end to end through the public API, from host arrays, nothing resident
+    e2e = None
+    if not args.no_e2e:
+        e2e_t = []
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            model.release_device()
+            D.TRANSFER["h2d"] = D.TRANSFER["d2h"] = 0
+            _lib.stats(reset=True)
+            barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            r2 = one_solve()
+            torch.cuda.synchronize()
+            e2e_t.append(time.perf_counter() - t)
+            _, lib_h2d = _lib.stats(reset=True)
+            h2d = D.TRANSFER["h2d"] + lib_h2d
+            d2h = D.TRANSFER["d2h"]
+        et = torch.tensor([float(np.mean(e2e_t))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(et.item()), "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "status": r2.status, "iterations": r2.iterations}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel (multifrontal refactorisation)
+    _, ws, backend = model._kkt_cache
+    info = backend.symbolic.info
+    nnz_k, nnz_l = info["nnz_a"], info["nnz_l"]
+    alg_bytes = 12 * nnz_k + 12 * nnz_l      # K values+indices in, L out
+    peak, peak_kind = _peaks()
+    ref = phases.get("refactor", {"mean_ms": float("nan"), "count": 0})
+    achieved = alg_bytes / (ref["mean_ms"] * 1e-3) / 1e9 if ref["count"] else None
+    per_iter = {k: v["total_ms"] / (args.steps * max(1, iters)) for k, v in phases.items()}
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            dt, orep = cpu_baseline(args.workload, args.tol, am)
+            cpu = {"value": dt, "unit": "s", "cores": 1, "kind": "port",
+                   "sample": f"one full {args.workload} solve to tol {args.tol:g} "
+                             f"({orep.iterations} iterations, objective {orep.objective:.10g}) by the "
+                             "oracle port, ordering injected (loop-fair)"}
+        except Exception as exc:  # never fail the bench line on the baseline leg
+            cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md Appendix B IEEE-14 tiling, no load perturbation)",
+        "config": {"workload": f"{args.workload}: {model.n_var} vars / {model.n_con} cons "
+                               f"({WORKLOADS[args.workload]} IEEE-14 tiles, limits), tol {args.tol:g}",
+                   "nnz_jac": model.nnz_jac, "nnz_hess": model.nnz_hess, "nnz_K": nnz_k,
+                   "nnz_L": nnz_l, "fronts": info["n_fronts"], "front_levels": info["n_levels"],
+                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
+                   "parallelism": "replicas" if world > 1 else "single instance"},
+        "iterations": iters, "objective": rep.objective, "status": rep.status,
+        "per_iter_ms": per_iter,
+        "roofline": {"bound": "hbm", "kernel": "mf_factor_kernel (refactor)",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                     "mean_launch_ms": ref["mean_ms"]},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clk,
+        "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -32,6 +32,8 @@ typedef struct gn_kkt gn_kkt;             /* KKT vector-kernel plan (A, W gather
 
 const char *gn_last_error(void);
 int gn_version(void);
+/* kernel launches and plan-upload bytes since the last reset */
+void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset);
 
 /* ------------------------------------------------------------------ */
 /* Host structure (CPU; no device needed)                              */
@@ -129,6 +131,8 @@ void gn_symbolic_destroy(gn_symbolic *sym);
 #define GN_AD_HESS 16u
 
 int gn_model_upload(gn_model *mdl);
+/* free the device copy of the plan (the host structure stays valid) */
+int gn_model_release(gn_model *mdl);
 /* Objective, constraints, gradient, Jacobian and Lagrangian Hessian values.
  * Replaces autodiff.py:45-142 (eval_*), with the _Problem scaling
  * (ipm.py:208-249) folded in: f *= obj_scale, c[i] *= con_scale[i],

@@ -58,6 +58,7 @@ class GridOpfError(RuntimeError):
 _SIGS = {
     "gn_last_error": (ctypes.c_char_p, []),
     "gn_version": (c_i32, []),
+    "gn_stats": (None, [P, P, c_i32]),
     "gn_canonical_order": (c_i32, [c_i64, c_i32, c_i32, P, P, P, P]),
     "gn_model_create": (c_i32, [P, c_i32, c_i64, c_i64, P]),
     "gn_model_info": (c_i32, [P, P, P, P]),
@@ -74,6 +75,7 @@ _SIGS = {
     "gn_symbolic_export": (c_i32, [P] * 9),
     "gn_symbolic_destroy": (None, [P]),
     "gn_model_upload": (c_i32, [P]),
+    "gn_model_release": (c_i32, [P]),
     "gn_ad_eval": (c_i32, [P, P, P, c_dbl, P, c_dbl, P, P, P, P, P, c_u32, P, P, P]),
     "gn_symbolic_upload": (c_i32, [P]),
     "gn_chol_factor": (c_i32, [P, P, P, P, P]),
@@ -115,6 +117,13 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def stats(reset: bool = False) -> tuple[int, int]:
+    """(kernel launches, plan-upload H2D bytes) counted by the library."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    lib().gn_stats(ctypes.byref(a), ctypes.byref(b), 1 if reset else 0)
+    return a.value, b.value
 
 
 def check(rc: int) -> None:

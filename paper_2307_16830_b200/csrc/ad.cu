@@ -320,13 +320,17 @@ __global__ void ad_objective_kernel(const int32_t *__restrict__ src, const int64
 
 }  // namespace
 
-Model::~Model() {
-  if (!uploaded) return;
-  void *ps[] = {d.blocks, d.tape, d.consts, d.slots, d.var_idx, d.params, d.targets, d.c_ptr,
-                d.grad_ptr, d.jac_ptr, d.hess_ptr, d.c_src, d.grad_src, d.jac_src, d.hess_src,
-                d.obj_src, d.jac_rows, d.obj_block_ptr};
+static void release_model(Model &M) {
+  if (!M.uploaded) return;
+  void *ps[] = {M.d.blocks, M.d.tape, M.d.consts, M.d.slots, M.d.var_idx, M.d.params, M.d.targets,
+                M.d.c_ptr, M.d.grad_ptr, M.d.jac_ptr, M.d.hess_ptr, M.d.c_src, M.d.grad_src,
+                M.d.jac_src, M.d.hess_src, M.d.obj_src, M.d.jac_rows, M.d.obj_block_ptr};
   for (void *p : ps) dev_free(p);
+  M.d = Model::Dev{};
+  M.uploaded = false;
 }
+
+Model::~Model() { release_model(*this); }
 
 static void upload_model(Model &M) {
   std::vector<DevBlock> db;
@@ -408,7 +412,7 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
   GN_REQUIRE(M.uploaded, "model not uploaded to the device");
   if (what & GN_AD_HESS) GN_REQUIRE(y != nullptr || M.m == 0, "Hessian needs multipliers");
   if (M.n_ctas_rec > 0)
-    ad_records_kernel<<<static_cast<unsigned>(M.n_ctas_rec), kRecThreads, 0, st>>>(
+    GN_LAUNCH(ad_records_kernel, static_cast<unsigned>(M.n_ctas_rec), kRecThreads, 0, st, 
         M.d.blocks, static_cast<int>(M.dblocks.size()), reinterpret_cast<const int4 *>(M.d.tape),
         M.d.consts, M.d.slots, M.d.var_idx, M.d.params, M.d.targets, x, y, con_scale, obj_w, what,
         contrib);
@@ -433,12 +437,12 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
   ga.nseg = ns;
   if (ns > 0) {
     int64_t tot = ga.begin[ns];
-    ad_gather_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(ga, contrib, flags);
+    GN_LAUNCH(ad_gather_kernel, static_cast<unsigned>((tot + 255) / 256), 256, 0, st, ga, contrib, flags);
     GN_LAUNCH_CHECK();
   }
   if (what & GN_AD_F) {
     if (M.d.n_obj_blocks > 0) {
-      ad_objective_kernel<<<1, 256, 0, st>>>(M.d.obj_src, M.d.obj_block_ptr, M.d.n_obj_blocks, contrib,
+      GN_LAUNCH(ad_objective_kernel, 1, 256, 0, st, M.d.obj_src, M.d.obj_block_ptr, M.d.n_obj_blocks, contrib,
                                              obj_scale, f, flags);
       GN_LAUNCH_CHECK();
     } else {
@@ -455,6 +459,10 @@ extern "C" int gn_model_upload(gn_model *M) {
   return guarded([&] {
     if (!M->uploaded) upload_model(*M);
   });
+}
+
+extern "C" int gn_model_release(gn_model *M) {
+  return guarded([&] { release_model(*M); });
 }
 
 extern "C" int gn_ad_eval(gn_model *M, const double *x, const double *y, double obj_weight,

@@ -1,12 +1,26 @@
-// Error reporting for the C-ABI (gridopf.h).
+// Error reporting and launch/transfer accounting for the C-ABI (gridopf.h).
+#include <atomic>
 #include <string>
 
 #include "internal.h"
 
 namespace gn {
 static thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+static std::atomic<int64_t> g_h2d{0};
 void set_error(const std::string &msg) { g_last_error = msg; }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_h2d(size_t bytes) { g_h2d.fetch_add(static_cast<int64_t>(bytes), std::memory_order_relaxed); }
 }  // namespace gn
 
 extern "C" const char *gn_last_error(void) { return gn::g_last_error.c_str(); }
 extern "C" int gn_version(void) { return 1; }
+
+extern "C" void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset) {
+  if (launches) *launches = gn::g_launches.load();
+  if (h2d_bytes) *h2d_bytes = gn::g_h2d.load();
+  if (reset) {
+    gn::g_launches.store(0);
+    gn::g_h2d.store(0);
+  }
+}

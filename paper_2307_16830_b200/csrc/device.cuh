@@ -19,12 +19,24 @@ namespace gn {
 
 #define GN_LAUNCH_CHECK() GN_CUDA(cudaGetLastError())
 
+// kernel launch + error check + launch accounting (gn_stats)
+#define GN_LAUNCH(kern, grid, block, smem, st, ...)     \
+  do {                                                  \
+    kern<<<grid, block, smem, st>>>(__VA_ARGS__);       \
+    ::gn::count_launch();                               \
+    GN_CUDA(cudaGetLastError());                        \
+  } while (0)
+
+void count_launch();
+void count_h2d(size_t bytes);
+
 template <class T>
 T *dev_upload(const std::vector<T> &v) {
   T *p = nullptr;
   size_t bytes = sizeof(T) * (v.empty() ? 1 : v.size());
   GN_CUDA(cudaMalloc(&p, bytes));
   if (!v.empty()) GN_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  count_h2d(sizeof(T) * v.size());
   return p;
 }
 

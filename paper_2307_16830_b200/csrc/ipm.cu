@@ -233,10 +233,10 @@ extern "C" int gn_ipm_prep(gn_kkt *K, const gn_ipm_vecs *v, int32_t n_mu, const 
     for (int k = 0; k < n_mu; ++k) ops_s[7 + k] = RED_MAX;
     GN_CUDA(cudaMemsetAsync(scal, 0, sizeof(double) * GN_PREP_DOUBLES, ST(stream)));
     if (K->n)
-      prep_x_kernel<<<red_grid(K->n), kRedThreads, 0, ST(stream)>>>(
+      GN_LAUNCH(prep_x_kernel, red_grid(K->n), kRedThreads, 0, ST(stream), 
           K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *v, mus, spec(*K, scal, 4 + n_mu, ops_x));
     if (K->m)
-      prep_s_kernel<<<red_grid(K->m), kRedThreads, 0, ST(stream)>>>(K->m, *v, mus,
+      GN_LAUNCH(prep_s_kernel, red_grid(K->m), kRedThreads, 0, ST(stream), K->m, *v, mus,
                                                                   spec(*K, scal + GN_PREP_S, 7 + n_mu, ops_s));
     GN_LAUNCH_CHECK();
   });
@@ -244,7 +244,7 @@ extern "C" int gn_ipm_prep(gn_kkt *K, const gn_ipm_vecs *v, int32_t n_mu, const 
 
 extern "C" int gn_ipm_pvec(gn_kkt *K, const gn_ipm_vecs *v, double mu, gn_vec7 *pv, void *stream) {
   return guarded([&] {
-    pvec_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, mu, *pv);
+    GN_LAUNCH(pvec_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, mu, *pv);
     GN_LAUNCH_CHECK();
   });
 }
@@ -253,7 +253,7 @@ extern "C" int gn_ipm_direction(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *
                                 double *scal, void *stream) {
   return guarded([&] {
     int ops[4] = {RED_MIN, RED_MIN, RED_MIN, RED_SUM};
-    direction_kernel<<<red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream)>>>(
+    GN_LAUNCH(direction_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), 
         K->n, K->m, *v, *steps, mu, tau, spec(*K, scal, 4, ops));
     GN_LAUNCH_CHECK();
   });
@@ -262,7 +262,7 @@ extern "C" int gn_ipm_direction(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *
 extern "C" int gn_ipm_trial_point(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                                   double *xt, double *st, void *stream) {
   return guarded([&] {
-    trial_point_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, *steps, alpha,
+    GN_LAUNCH(trial_point_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps, alpha,
                                                                                xt, st);
     GN_LAUNCH_CHECK();
   });
@@ -272,7 +272,7 @@ extern "C" int gn_ipm_trial_merit(gn_kkt *K, const gn_ipm_vecs *v, const double 
                                   const double *st, double *scal, void *stream) {
   return guarded([&] {
     int ops[5] = {RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
-    trial_merit_kernel<<<red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream)>>>(
+    GN_LAUNCH(trial_merit_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), 
         K->n, K->m, *v, ct, xt, st, spec(*K, scal, 5, ops));
     GN_LAUNCH_CHECK();
   });
@@ -281,7 +281,7 @@ extern "C" int gn_ipm_trial_merit(gn_kkt *K, const gn_ipm_vecs *v, const double 
 extern "C" int gn_ipm_accept(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                              double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream) {
   return guarded([&] {
-    accept_kernel<<<ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream)>>>(K->n, K->m, *v, *steps, alpha,
+    GN_LAUNCH(accept_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps, alpha,
                                                                           alpha_z, mu, kappa_sigma, flags);
     GN_LAUNCH_CHECK();
   });

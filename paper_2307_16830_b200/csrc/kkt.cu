@@ -415,7 +415,7 @@ extern "C" int gn_kkt_sigma(int64_t len, const double *dl, const double *du, con
                             const double *zu, double *sigma, void *stream) {
   return guarded([&] {
     if (len == 0) return;
-    sigma_kernel<<<blocks_for(len), kT, 0, ST(stream)>>>(len, dl, du, zl, zu, sigma);
+    GN_LAUNCH(sigma_kernel, blocks_for(len), kT, 0, ST(stream), len, dl, du, zl, zu, sigma);
     GN_LAUNCH_CHECK();
   });
 }
@@ -424,11 +424,11 @@ extern "C" int gn_kkt_matvec(gn_kkt *K, int kind, const double *vals, const doub
                              void *stream) {
   return guarded([&] {
     if (kind == 0 && K->n)
-      w_matvec_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, vals, v, out);
+      GN_LAUNCH(w_matvec_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, vals, v, out);
     else if (kind == 1 && K->m)
-      a_matvec_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, vals, v, out);
+      GN_LAUNCH(a_matvec_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, vals, v, out);
     else if (kind == 2 && K->n)
-      at_matvec_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, vals, v, out);
+      GN_LAUNCH(at_matvec_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, vals, v, out);
     GN_LAUNCH_CHECK();
   });
 }
@@ -437,7 +437,7 @@ extern "C" int gn_kkt_assemble(gn_kkt *K, const gn_kkt_state *st, double *kvals,
   return guarded([&] {
     GN_REQUIRE(K->has_assembly, "KKT plan built without the condensed structure");
     if (K->nk == 0) return;
-    assemble_kernel<<<blocks_for(K->nk), kT, 0, ST(stream)>>>(K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1, K->d.k_s2,
+    GN_LAUNCH(assemble_kernel, blocks_for(K->nk), kT, 0, ST(stream), K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1, K->d.k_s2,
                                                             K->d.k_w, K->d.k_diag, *st, kvals);
     GN_LAUNCH_CHECK();
   });
@@ -447,9 +447,9 @@ extern "C" int gn_kkt_condense_rhs(gn_kkt *K, const gn_kkt_state *st, const gn_v
                                    double *qs, double *qy, double *rhs, void *stream) {
   return guarded([&] {
     if (K->m)
-      rhs_rows_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, *st, *pv, qs, qy, K->d.scratch);
+      GN_LAUNCH(rhs_rows_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, *st, *pv, qs, qy, K->d.scratch);
     if (K->n)
-      rhs_cols_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *st, *pv,
+      GN_LAUNCH(rhs_cols_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *st, *pv,
                                                              K->d.scratch, qx, rhs);
     GN_LAUNCH_CHECK();
   });
@@ -460,7 +460,7 @@ extern "C" int gn_kkt_recover_slack_dual(gn_kkt *K, const gn_kkt_state *st, cons
                                          void *stream) {
   return guarded([&] {
     if (K->m)
-      recover_sd_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, *st, dx, qs, qy,
+      GN_LAUNCH(recover_sd_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, *st, dx, qs, qy,
                                                                ds, dy);
     GN_LAUNCH_CHECK();
   });
@@ -471,10 +471,10 @@ extern "C" int gn_kkt_recover_bound_duals(gn_kkt *K, const gn_kkt_state *st, con
                                           double *dzsl, double *dzsu, int32_t *flags, void *stream) {
   return guarded([&] {
     if (K->n)
-      recover_bd_kernel<<<blocks_for(K->n), kT, 0, ST(stream)>>>(K->n, st->dxl, st->dxu, st->zxl, st->zxu, pv->zxl,
+      GN_LAUNCH(recover_bd_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, st->dxl, st->dxu, st->zxl, st->zxu, pv->zxl,
                                                                pv->zxu, dx, dzxl, dzxu, flags);
     if (K->m)
-      recover_bd_kernel<<<blocks_for(K->m), kT, 0, ST(stream)>>>(K->m, st->dsl, st->dsu, st->zsl, st->zsu, pv->zsl,
+      GN_LAUNCH(recover_bd_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, st->dsl, st->dsu, st->zsl, st->zsu, pv->zsl,
                                                                pv->zsu, ds, dzsl, dzsu, flags);
     GN_LAUNCH_CHECK();
   });
@@ -486,17 +486,17 @@ extern "C" int gn_kkt_residual(gn_kkt *K, const gn_kkt_state *st, const gn_vec7 
     // norm[0..2): per-side maxima, combined into norm[0]
     RedSpec rx = max_spec(*K, norm);
     if (K->n)
-      residual_x_kernel<<<red_grid(K->n), kRedThreads, 0, ST(stream)>>>(K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, K->d.at_ptr,
+      GN_LAUNCH(residual_x_kernel, red_grid(K->n), kRedThreads, 0, ST(stream), K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, K->d.at_ptr,
                                                                K->d.at_p, K->d.at_row, *st, *steps, *pv, *res, rx);
     else
       GN_CUDA(cudaMemsetAsync(norm, 0, sizeof(double), ST(stream)));
     RedSpec rs = max_spec(*K, norm + 1);
     if (K->m)
-      residual_s_kernel<<<red_grid(K->m), kRedThreads, 0, ST(stream)>>>(K->m, K->d.a_rowptr, K->d.a_col, *st, *steps, *pv,
+      GN_LAUNCH(residual_s_kernel, red_grid(K->m), kRedThreads, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, *st, *steps, *pv,
                                                                *res, rs);
     else
       GN_CUDA(cudaMemsetAsync(norm + 1, 0, sizeof(double), ST(stream)));
-    max2_kernel<<<1, 1, 0, ST(stream)>>>(norm, norm + 1, norm);
+    GN_LAUNCH(max2_kernel, 1, 1, 0, ST(stream), norm, norm + 1, norm);
     GN_LAUNCH_CHECK();
   });
 }
@@ -505,7 +505,7 @@ extern "C" int gn_kkt_matrix_scale(gn_kkt *K, const gn_kkt_state *st, double *ou
   return guarded([&] {
     int64_t big = std::max(std::max(K->n, K->m), std::max(K->nh, K->nj));
     RedSpec r = max_spec(*K, out);
-    matrix_scale_kernel<<<red_grid(big, 4), kRedThreads, 0, ST(stream)>>>(K->n, K->m, K->nh, K->nj, *st, r);
+    GN_LAUNCH(matrix_scale_kernel, red_grid(big, 4), kRedThreads, 0, ST(stream), K->n, K->m, K->nh, K->nj, *st, r);
     GN_LAUNCH_CHECK();
   });
 }
@@ -514,7 +514,7 @@ extern "C" int gn_vec7_axpy(gn_kkt *K, gn_vec7 *y, const gn_vec7 *x, double alph
   return guarded([&] {
     int64_t len = std::max(K->n, K->m);
     if (len == 0) return;
-    axpy7_kernel<<<blocks_for(len), kT, 0, ST(stream)>>>(K->n, K->m, *y, *x, alpha);
+    GN_LAUNCH(axpy7_kernel, blocks_for(len), kT, 0, ST(stream), K->n, K->m, *y, *x, alpha);
     GN_LAUNCH_CHECK();
   });
 }

@@ -22,12 +22,19 @@ def stream_ptr(stream=None) -> int:
     return s.cuda_stream
 
 
+TRANSFER = {"h2d": 0, "d2h": 0}   # bytes moved by these helpers (bench accounting)
+
+
 def to_dev(a, dtype=torch.float64):
     """numpy / list / tensor -> contiguous CUDA tensor of ``dtype``."""
     dev = require_cuda()
     if isinstance(a, torch.Tensor):
+        if a.device.type != "cuda":
+            TRANSFER["h2d"] += a.numel() * a.element_size()
         return a.to(device=dev, dtype=dtype).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev)
+    t = torch.as_tensor(np.ascontiguousarray(a), dtype=dtype, device=dev)
+    TRANSFER["h2d"] += t.numel() * t.element_size()
+    return t
 
 
 def empty(n, dtype=torch.float64):
@@ -43,4 +50,5 @@ def is_tensor(a) -> bool:
 
 
 def to_host(t) -> np.ndarray:
+    TRANSFER["d2h"] += t.numel() * t.element_size()
     return t.detach().cpu().numpy()

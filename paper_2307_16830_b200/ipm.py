@@ -28,6 +28,7 @@ from .autodiff import C, F, GRAD, HESS, JAC, NonFiniteResult, evaluator
 from .kkt import (CondensedBackend, DegenerateInterior, KKTWorkspace, PVec, RegState,
                   RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
                   solve_with_regularization)
+from .profiling import span
 
 OPTIMAL = "optimal"
 MAX_ITER = "max_iter"
@@ -254,6 +255,7 @@ class _DeviceSolve:
 
     def read(self, lo, hi):
         """Copy scal[lo:hi] and both flag words to the host (one stream sync)."""
+        D.TRANSFER["d2h"] += 8 * (hi - lo) + 8
         self.host[lo:hi].copy_(self.scal[lo:hi], non_blocking=True)
         self.host_flags.copy_(self.flags, non_blocking=True)
         torch.cuda.current_stream().synchronize()
@@ -279,10 +281,20 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     stream = D.stream_ptr()
     timer = _Timer()
 
-    ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols)
+    # symbolic analysis (condensed pattern, ordering, symbolic factor, device
+    # plans) is a function of the sparsity only: cached on the model
+    key = None if opts.ordering is None else id(opts.ordering)
+    cache = getattr(model, "_kkt_cache", None)
+    if cache is None or cache[0] != key:
+        ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols)
+        backend = CondensedBackend(ws, ordering=opts.ordering)
+        model._kkt_cache = (key, ws, backend)
+    else:
+        _, ws, backend = cache
+        backend.n_factorizations = 0
     # the workspace reads the solver's duals in place (no copies per iteration)
     ws.zxl, ws.zxu, ws.zsl, ws.zsu = P.zxl, P.zxu, P.zsl, P.zsu
-    backend = CondensedBackend(ws, ordering=opts.ordering)
+    ws.delta_w = ws.delta_c = 0.0
     reg = RegState()
     V = P.vecs(ws)
     ev = P.ev
@@ -352,14 +364,17 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         # ---- derivatives at x (ipm.py:384-391)
         ev_flags.zero_()
         t0 = timer.start()
-        ev.launch(P.x, F | C | GRAD | JAC | HESS, y=P.y, obj_weight=P.obj_scale,
-                  con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
-                  grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
+        with span("ad_full"):
+            ev.launch(P.x, F | C | GRAD | JAC | HESS, y=P.y, obj_weight=P.obj_scale,
+                      con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
+                      grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
         timer.stop("ad", t0)
         # ---- widths, Sigma, residual blocks and reductions (ipm.py:393-429)
         cands = _mu_candidates(mu, mu_min, opts, L.IPM_MAX_MU)
         mus = (ctypes.c_double * len(cands))(*cands)
-        L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal), stream))
+        with span("prep"):
+            L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal),
+                                    stream))
         P.flags[0:1].copy_(ev_flags)
         sc, adf, ipf = P.read(0, 49)
         check_ipm_flags(ipf)
@@ -433,8 +448,9 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
                                            L.ptr(P.xt), L.ptr(P.st), stream))
             ev_flags.zero_()
             t0 = timer.start()
-            ev.launch(P.xt, F | C, con_scale=P.con_scale, obj_scale=P.obj_scale,
-                      f=P.scal[49:50], c=P.ct)
+            with span("ad_trial"):
+                ev.launch(P.xt, F | C, con_scale=P.con_scale, obj_scale=P.obj_scale,
+                          f=P.scal[49:50], c=P.ct)
             timer.stop("ad", t0)
             L.check(lib.gn_ipm_trial_merit(ws.handle, ctypes.byref(V), L.ptr(P.ct), L.ptr(P.xt),
                                            L.ptr(P.st), L.ptr(P.scal[54:59]), stream))

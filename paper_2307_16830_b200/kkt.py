@@ -24,6 +24,7 @@ import torch
 from . import _lib as L
 from . import device as D
 from . import sparse as S
+from .profiling import span
 
 DELTA_W_INIT = 1e-4
 DELTA_W_MIN = 1e-20
@@ -102,9 +103,12 @@ class CondensedStructure:
     handle: object = None
 
     def __del__(self):
-        if self.handle is not None and L._lib is not None:
-            L.lib().gn_condense_destroy(self.handle)
-            self.handle = None
+        try:
+            if self.handle is not None and L._lib is not None:
+                L.lib().gn_condense_destroy(self.handle)
+        except Exception:
+            pass
+        self.handle = None
 
 
 def symbolic_condense(hess_rows, hess_cols, jac_rows, jac_cols, n) -> CondensedStructure:
@@ -165,9 +169,12 @@ class KKTWorkspace:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and L._lib is not None:
-            L.lib().gn_kkt_destroy(h)
-            self.handle = None
+        try:
+            if h is not None and L._lib is not None:
+                L.lib().gn_kkt_destroy(h)
+        except Exception:
+            pass
+        self.handle = None
 
     # -- state -------------------------------------------------------------
     def set_iterate(self, w_vals, a_vals, dxl, dxu, zxl, zxu, dsl, dsu, zsl, zsu):
@@ -304,13 +311,15 @@ class CondensedBackend:
 
     def assemble(self) -> None:
         st = self.ws.state()
-        L.check(L.lib().gn_kkt_assemble(self.ws.handle, ctypes.byref(st), L.ptr(self.kvals),
-                                        D.stream_ptr()))
+        with span("assemble"):
+            L.check(L.lib().gn_kkt_assemble(self.ws.handle, ctypes.byref(st), L.ptr(self.kvals),
+                                            D.stream_ptr()))
 
     def factorize_async(self):
         self.assemble()
         self.n_factorizations += 1
-        self.factor = S.factorize_device(self.symbolic, self.kvals, self.fws)
+        with span("refactor"):
+            self.factor = S.factorize_device(self.symbolic, self.kvals, self.fws)
         return self.factor
 
     def try_factorize(self) -> bool:
@@ -326,9 +335,12 @@ class CondensedBackend:
     def solve_pvec(self, pv: PVec):
         """Fused condense_pvec + solve3 for the solver's hot path."""
         ws = self.ws
-        qx, qs, qy, rhs = ws._condense(pv)
-        dx = S.solve_device(self.factor, rhs, D.empty(ws.n))
-        ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
+        with span("rhs"):
+            qx, qs, qy, rhs = ws._condense(pv)
+        with span("solve"):
+            dx = S.solve_device(self.factor, rhs, D.empty(ws.n))
+        with span("recover"):
+            ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
         return dx, ds, dy
 
 

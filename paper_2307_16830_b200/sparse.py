@@ -136,9 +136,12 @@ class SymbolicFactorization:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and L._lib is not None:
-            L.lib().gn_symbolic_destroy(h)
-            self._h = None
+        try:
+            if h is not None and L._lib is not None:
+                L.lib().gn_symbolic_destroy(h)
+        except Exception:
+            pass
+        self._h = None
 
 
 def symbolic_cholesky(matrix: SparseSymmetric, perm=None) -> SymbolicFactorization:
