@@ -364,12 +364,23 @@ static void front_plan(Symbolic &S) {
     maxl = std::max<int64_t>(maxl, S.level[J]);
   }
   S.n_levels = nf ? maxl + 1 : 0;
+  // warp tasks: fronts of <= kWarpFrontRows rows whose whole subtree is small
+  // (children precede parents in index order, so one pass suffices)
+  std::vector<char> small(nf, 0);
+  for (int64_t J = 0; J < nf; ++J) {
+    bool ok = S.f_nrows[J] <= kWarpFrontRows;
+    for (int32_t t = S.f_child_ptr[J]; ok && t < S.f_child_ptr[J + 1]; ++t) ok = small[S.f_child[t]];
+    small[J] = ok;
+  }
+  // task order: small fronts by level, then the other fronts by level
   S.order.resize(nf);
+  S.nf_small = 0;
   {
-    std::vector<int64_t> lc(S.n_levels + 1, 0);
-    for (int64_t J = 0; J < nf; ++J) lc[S.level[J] + 1]++;
-    for (int64_t l = 0; l < S.n_levels; ++l) lc[l + 1] += lc[l];
-    for (int64_t J = 0; J < nf; ++J) S.order[lc[S.level[J]]++] = static_cast<int32_t>(J);
+    std::vector<int64_t> lc(2 * S.n_levels + 1, 0);
+    auto bucket = [&](int64_t J) { return (small[J] ? 0 : S.n_levels) + S.level[J]; };
+    for (int64_t J = 0; J < nf; ++J) lc[bucket(J) + 1]++, S.nf_small += small[J];
+    for (int64_t l = 0; l < 2 * S.n_levels; ++l) lc[l + 1] += lc[l];
+    for (int64_t J = 0; J < nf; ++J) S.order[lc[bucket(J)]++] = static_cast<int32_t>(J);
   }
 }
 

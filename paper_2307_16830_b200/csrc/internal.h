@@ -127,6 +127,18 @@ struct Condense {
 };
 
 // ------------------------------------------------------- symbolic factor
+constexpr int kWarpFrontRows = 32;   // fronts this small are factored by one warp
+
+// device record of one front (loaded with four 16-byte loads)
+struct alignas(16) FrontMeta {
+  int64_t f_off;      // front storage (doubles), s x s column-major
+  int64_t a_begin;    // first entry of the front's A scatter
+  int32_t a_count;
+  int32_t first, ncols, nrows;
+  int32_t parent, child_begin, child_end, v_off;
+  int32_t rows_off, relmap_off, pad;
+};
+
 struct Symbolic {
   int64_t n = 0, nnz_a = 0;
   std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, row_cols,
@@ -143,7 +155,8 @@ struct Symbolic {
   std::vector<int32_t> relmap;                 // child update rows -> parent local rows
   std::vector<int64_t> f_a_ptr;                // CSR A scatter per front
   std::vector<int64_t> a_kslot, a_fpos;        // (kvals slot, F offset)
-  std::vector<int32_t> order;                  // task order, leaves first
+  std::vector<int32_t> order;                  // task order: [small by level | large by level]
+  int64_t nf_small = 0;                        // warp-task fronts (prefix of order)
   std::vector<int32_t> level;
   std::vector<int64_t> l_export;               // reference L slot -> F offset
   int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
@@ -151,20 +164,15 @@ struct Symbolic {
   // device
   bool uploaded = false;
   struct Dev {
-    int32_t *f_first = nullptr, *f_ncols = nullptr, *f_nrows = nullptr, *f_parent = nullptr;
-    int64_t *f_rows_off = nullptr;
+    FrontMeta *meta = nullptr;        // per-front metadata (one 64-byte record)
     int32_t *f_rows = nullptr;
-    int64_t *f_off = nullptr, *f_voff = nullptr;
-    int32_t *f_child_ptr = nullptr, *f_child = nullptr;
-    int64_t *f_relmap_off = nullptr;
+    int32_t *f_child = nullptr;
     int32_t *relmap = nullptr;
-    int64_t *f_a_ptr = nullptr;
     int32_t *a_kslot = nullptr;
-    int64_t *a_fpos = nullptr;
+    int32_t *a_loc = nullptr;
     int32_t *order = nullptr;
     int32_t *nchild = nullptr;        // template counters
     int32_t *counters = nullptr;      // scratch counters
-    int32_t *task = nullptr;          // task queue heads
     int64_t *l_export = nullptr;
     int64_t *perm = nullptr;          // internal position -> original index
   } d;

@@ -43,8 +43,9 @@ inline int red_grid(int64_t n, int per_thread = 1) {
 }
 
 // Reduce vals[0..spec.k) held by every thread of the grid (blockDim ==
-// kRedThreads); thread 0 of the last CTA writes spec.out.  Must be reached
-// by all threads of every CTA.
+// kRedThreads); the last CTA to finish writes spec.out.  Must be reached by
+// all threads of every CTA.  Every combine happens in a fixed position (lane
+// strides and shuffle trees), so results are bitwise run-to-run identical.
 template <int K>
 __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
   __shared__ double sh[K][kRedThreads / 32];
@@ -58,27 +59,30 @@ __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
     if (lane == 0) sh[k][warp] = v;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 0; k < spec.k; ++k) {
-      double v = sh[k][0];
-      for (int w = 1; w < nw; ++w) v = red_combine(spec.op[k], v, sh[k][w]);
-      spec.partials[blockIdx.x * kRedMaxSlots + k] = v;
-    }
+  if (threadIdx.x < spec.k) {   // one thread per slot combines the warps
+    const int k = threadIdx.x;
+    double v = sh[k][0];
+    for (int w = 1; w < nw; ++w) v = red_combine(spec.op[k], v, sh[k][w]);
+    spec.partials[blockIdx.x * kRedMaxSlots + k] = v;
     __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
     unsigned int done = atomicAdd(spec.counter, 1u);
     last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    for (int k = 0; k < spec.k; ++k) {
-      double v = __ldcg(spec.partials + k);
-      for (unsigned b = 1; b < gridDim.x; ++b)
-        v = red_combine(spec.op[k], v, __ldcg(spec.partials + b * kRedMaxSlots + k));
-      spec.out[k] = v;
-    }
-    *spec.counter = 0u;
+  if (!last) return;
+  __threadfence();
+  for (int k = warp; k < spec.k; k += nw) {   // one warp per slot over the CTA partials
+    const int op = spec.op[k];
+    double v = red_identity(op);
+    for (unsigned b = lane; b < gridDim.x; b += 32)
+      v = red_combine(op, v, __ldcg(spec.partials + b * kRedMaxSlots + k));
+    for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_down_sync(0xffffffffu, v, o));
+    if (lane == 0) spec.out[k] = v;
   }
+  if (threadIdx.x == 0) *spec.counter = 0u;
 }
 
 }  // namespace gn

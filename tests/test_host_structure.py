@@ -150,3 +150,18 @@ def test_larger_grid_structure_matches_oracle():
     osym = OS.symbolic(ocs.matrix, perm)
     np.testing.assert_array_equal(sym.l_rowidx, osym.l_rowidx)
     np.testing.assert_array_equal(sym.parent, osym.parent)
+
+
+def test_min_degree_matches_shipped_reference_at_2k_buses():
+    """C2 (143 tiles, 17,922 columns): the permutation is bit-identical to the
+    reference's own O(n^2) amd_order (amd.py:18-54), run by
+    tests/golden/make_perm_golden.py."""
+    import os
+
+    from conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "C2_perm.npz"))
+    m = build_acopf(parse_matpower(tiled_case(143))).model
+    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
+    assert cs.matrix.indices.size == int(g["nnz_k"])
+    np.testing.assert_array_equal(sparse.amd_order(cs.matrix), g["perm"].astype(np.int64))
