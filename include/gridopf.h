@@ -117,6 +117,11 @@ int gn_symbolic_info(const gn_symbolic *sym, gn_symbolic_info_t *info);
 int gn_symbolic_export(const gn_symbolic *sym, int64_t *parent, int64_t *a_rowptr,
                        int64_t *a_rowcol, int64_t *a_srcslot, int64_t *row_ptr,
                        int64_t *row_cols, int64_t *l_colptr, int64_t *l_rowidx);
+/* Supernodal front plan (n_fronts entries each): first column, width,
+ * rows, parent front (-1 = root), task order; *nf_small = number of
+ * warp-task fronts (a prefix of order). */
+int gn_symbolic_fronts(const gn_symbolic *sym, int32_t *first, int32_t *ncols, int32_t *nrows,
+                       int32_t *parent, int32_t *order, int64_t *nf_small);
 void gn_symbolic_destroy(gn_symbolic *sym);
 
 /* ------------------------------------------------------------------ */
@@ -156,6 +161,10 @@ int gn_chol_factor(gn_symbolic *sym, const double *kvals, double *fronts,
  * Replaces _solve_kernel/solve (cholesky.py:175-217). */
 int gn_chol_solve(gn_symbolic *sym, const double *fronts, const double *b, double *x,
                   double *ws, void *stream);
+/* Diagnostics: when trace (device int64[3][n_fronts][4]) is non-NULL the
+ * factor / forward / backward kernels stamp %globaltimer per front (task
+ * start, dependencies met, assembled, done).  NULL turns it off. */
+int gn_chol_set_trace(gn_symbolic *sym, int64_t *trace);
 /* Factor values in the reference CSC layout (l_colptr/l_rowidx). */
 int gn_chol_export_l(gn_symbolic *sym, const double *fronts, double *l_vals, void *stream);
 

@@ -296,7 +296,8 @@ static void front_plan(Symbolic &S) {
     if (S.parent[l] != -1) S.f_parent[J] = snode_of[S.parent[l]];
     for (int64_t c = 0; c < w; ++c) S.flops += (s - c - 1) * (s - c - 1) + 2 * (s - c);
   }
-  S.front_doubles = S.f_off[nf];
+  S.dinv_off = S.f_off[nf];                // 1 / L[k][k] per column, after the fronts
+  S.front_doubles = S.f_off[nf] + n;
   S.vec_doubles = S.f_voff[nf];
   // children CSR (increasing child index)
   S.f_child_ptr.assign(nf + 1, 0);
@@ -498,6 +499,18 @@ extern "C" int gn_symbolic_export(const gn_symbolic *S, int64_t *parent, int64_t
     copy_out(row_cols, S->row_cols);
     copy_out(l_colptr, S->l_colptr);
     copy_out(l_rowidx, S->l_rowidx);
+  });
+}
+
+extern "C" int gn_symbolic_fronts(const gn_symbolic *S, int32_t *first, int32_t *ncols, int32_t *nrows,
+                                  int32_t *parent, int32_t *order, int64_t *nf_small) {
+  return guarded([&] {
+    copy_out(first, S->f_first);
+    copy_out(ncols, S->f_ncols);
+    copy_out(nrows, S->f_nrows);
+    copy_out(parent, S->f_parent);
+    copy_out(order, S->order);
+    if (nf_small) *nf_small = S->nf_small;
   });
 }
 

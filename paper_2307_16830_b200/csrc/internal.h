@@ -159,8 +159,10 @@ struct Symbolic {
   int64_t nf_small = 0;                        // warp-task fronts (prefix of order)
   std::vector<int32_t> level;
   std::vector<int64_t> l_export;               // reference L slot -> F offset
+  int64_t dinv_off = 0;   // fronts buffer: [fronts | inverse diagonal (n)]
   int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
   int64_t flops = 0;
+  long long *trace = nullptr;   // optional device [3][nf][4] timing stamps
   // device
   bool uploaded = false;
   struct Dev {

@@ -267,3 +267,35 @@ def estimate_condition(factor: NumericFactor, matrix: SparseSymmetric) -> float:
         x = np.zeros(n)
         x[j] = 1.0
     return norm_a * est
+
+
+def front_plan(symbolic: SymbolicFactorization) -> dict:
+    """The supernodal front plan of a symbolic factorisation (diagnostics)."""
+    nf = symbolic.info["n_fronts"]
+    out = {k: np.empty(nf, np.int32) for k in ("first", "ncols", "nrows", "parent", "order")}
+    nsm = ctypes.c_int64()
+    L.check(L.lib().gn_symbolic_fronts(symbolic._h, *(L.ptr(out[k]) for k in
+                                                      ("first", "ncols", "nrows", "parent", "order")),
+                                       ctypes.byref(nsm)))
+    out["nf_small"] = nsm.value
+    return out
+
+
+def trace_factor_solve(symbolic: SymbolicFactorization, kvals: torch.Tensor, b: torch.Tensor):
+    """Run one refactorisation and one solve with per-front %globaltimer
+    stamps; returns int64 [3][n_fronts][4] (factor, forward, backward) of
+    (start, dependencies met, assembled, done) in ns (0 = not stamped), and
+    [64][5] panel stamps of the last front (start, loaded, diagonal block,
+    TRSM, trailing update)."""
+    nf = symbolic.info["n_fronts"]
+    tr = torch.zeros(3 * nf * 4 + 64 * 5, dtype=torch.int64, device=kvals.device)
+    h = symbolic.handle()
+    L.check(L.lib().gn_chol_set_trace(h, L.ptr(tr)))
+    try:
+        f = factorize_device(symbolic, kvals)
+        solve_device(f, b.clone())
+        torch.cuda.synchronize()
+    finally:
+        L.check(L.lib().gn_chol_set_trace(h, None))
+    t = tr.cpu().numpy()
+    return t[:12 * nf].reshape(3, nf, 4), t[12 * nf:].reshape(64, 5)
