@@ -79,29 +79,53 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
 }
 
 // ------------------------------------------------------------ ordering
+// Explicit elimination graph exactly as the reference builds it: eliminating
+// v turns its neighbourhood nb into a clique, adj[u] = adj[u] - {v} + nb - {u}
+// for u in nb, degree[u] = |adj[u]|.  Adjacency lists are unsorted; set
+// union uses two stamp arrays, so one elimination costs
+// sum_{u in nb} (|adj[u]| + |nb|) cheap operations.  Selection uses a heap
+// keyed (degree, initial degree, index) with lazy deletion, which is the
+// reference's strict-< scan order.
 static void min_degree(int64_t n, const int64_t *indptr, const int64_t *indices, int64_t *perm) {
   std::vector<std::vector<int32_t>> adj(n);
-  for (int64_t j = 0; j < n; ++j)
-    for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
-      int64_t i = indices[p];
-      if (i != j) {
-        adj[i].push_back(static_cast<int32_t>(j));
-        adj[j].push_back(static_cast<int32_t>(i));
+  {
+    std::vector<int32_t> cnt(n, 0);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p)
+        if (indices[p] != j) cnt[indices[p]]++, cnt[j]++;
+    for (int64_t v = 0; v < n; ++v) adj[v].reserve(cnt[v]);
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
+        const int64_t i = indices[p];
+        if (i != j) {
+          adj[i].push_back(static_cast<int32_t>(j));
+          adj[j].push_back(static_cast<int32_t>(i));
+        }
       }
+    // duplicate coordinates are not expected in a CSC pattern, but keep set
+    // semantics if they occur
+    std::vector<int64_t> seen(n, -1);
+    for (int64_t v = 0; v < n; ++v) {
+      auto &a = adj[v];
+      size_t w = 0;
+      for (int32_t x : a)
+        if (seen[x] != v) seen[x] = v, a[w++] = x;
+      a.resize(w);
     }
-  for (auto &a : adj) {
-    std::sort(a.begin(), a.end());
-    a.erase(std::unique(a.begin(), a.end()), a.end());
   }
   std::vector<int64_t> deg(n), deg0(n);
   std::vector<char> alive(n, 1);
   using Key = std::tuple<int64_t, int64_t, int64_t>;
-  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap;
+  std::vector<Key> hv;
+  hv.reserve(static_cast<size_t>(n) * 4);
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> heap(std::greater<Key>(), std::move(hv));
   for (int64_t v = 0; v < n; ++v) {
     deg[v] = deg0[v] = static_cast<int64_t>(adj[v].size());
     heap.emplace(deg[v], deg0[v], v);
   }
-  std::vector<int32_t> merged;
+  std::vector<int64_t> in_nb(n, -1);    // == k: member of the current pivot's nb
+  std::vector<int64_t> in_adj(n, -1);   // == stamp: member of adj[u] (current u)
+  int64_t stamp = 0;
   for (int64_t k = 0; k < n; ++k) {
     int64_t v;
     for (;;) {
@@ -116,28 +140,28 @@ static void min_degree(int64_t n, const int64_t *indptr, const int64_t *indices,
     alive[v] = 0;
     std::vector<int32_t> nb;
     nb.swap(adj[v]);
-    // clique formation (amd.py:49-53): adj[u] = adj[u] | nb  minus {u, v}
+    const int64_t dnb = static_cast<int64_t>(nb.size());
+    for (int32_t x : nb) in_nb[x] = k;
     for (int32_t u : nb) {
       auto &au = adj[u];
-      merged.clear();
-      merged.reserve(au.size() + nb.size());
-      size_t a = 0, b = 0;
-      while (a < au.size() || b < nb.size()) {
-        int32_t x;
-        if (b == nb.size() || (a < au.size() && au[a] < nb[b])) {
-          x = au[a++];
-        } else if (a == au.size() || nb[b] < au[a]) {
-          x = nb[b++];
-        } else {
-          x = au[a++];
-          ++b;
+      ++stamp;
+      size_t w = 0;
+      int64_t present = 0;
+      for (int32_t x : au) {
+        if (x == v) continue;
+        au[w++] = x;
+        if (in_nb[x] == k) {
+          ++present;
+          in_adj[x] = stamp;
         }
-        if (x != u && x != v) merged.push_back(x);
       }
-      au.swap(merged);
+      au.resize(w);
+      if (present < dnb - 1)   // nb - {u} not yet contained: append the missing
+        for (int32_t x : nb)
+          if (x != u && in_adj[x] != stamp) au.push_back(x);
     }
     for (int32_t u : nb) {
-      int64_t nd = static_cast<int64_t>(adj[u].size());
+      const int64_t nd = static_cast<int64_t>(adj[u].size());
       if (nd != deg[u]) {
         deg[u] = nd;
         heap.emplace(nd, deg0[u], u);
@@ -298,7 +322,8 @@ static void front_plan(Symbolic &S) {
   }
   S.dinv_off = S.f_off[nf];                // 1 / L[k][k] per column, after the fronts
   S.front_doubles = S.f_off[nf] + n;
-  S.vec_doubles = S.f_voff[nf];
+  S.xp_off = S.f_voff[nf];
+  S.vec_doubles = S.f_voff[nf] + n;
   // children CSR (increasing child index)
   S.f_child_ptr.assign(nf + 1, 0);
   for (int64_t J = 0; J < nf; ++J)

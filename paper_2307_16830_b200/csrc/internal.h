@@ -160,6 +160,7 @@ struct Symbolic {
   std::vector<int32_t> level;
   std::vector<int64_t> l_export;               // reference L slot -> F offset
   int64_t dinv_off = 0;   // fronts buffer: [fronts | inverse diagonal (n)]
+  int64_t xp_off = 0;     // solve workspace: [front vectors | permuted vector (n)]
   int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
   int64_t flops = 0;
   long long *trace = nullptr;   // optional device [3][nf][4] timing stamps
@@ -167,6 +168,7 @@ struct Symbolic {
   bool uploaded = false;
   struct Dev {
     FrontMeta *meta = nullptr;        // per-front metadata (one 64-byte record)
+    void *cinfo = nullptr;            // per child edge: the child's extend-add fields
     int32_t *f_rows = nullptr;
     int32_t *f_child = nullptr;
     int32_t *relmap = nullptr;
