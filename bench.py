@@ -168,7 +168,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="C3", choices=tuple(WORKLOADS))
@@ -209,13 +209,16 @@ def main():
             dist.all_gather(bufs, x)
         return rep
 
+    # clocks are sampled from before the warm-up through the timed region
+    # (nvidia-smi needs ~1 s before its first sample)
+    clocks = _clock_sampler() if rank == 0 else None
+    time.sleep(1.0)
     for _ in range(max(args.warmup, 1)):
         rep = one_solve()
     # ---- timed region: device-resident solves
     _lib.stats(reset=True)
     profiling.reset()
     profiling.enable(True)
-    clocks = _clock_sampler() if rank == 0 else None
     step_ms = []
     barrier()
     torch.cuda.synchronize()

@@ -16,23 +16,48 @@
 
 namespace gn {
 
-// keys (col << 32 | row) -> sorted unique + inverse map
-static void csc_from_keys(int64_t n, const std::vector<uint64_t> &keys, std::vector<int64_t> &indptr,
-                          std::vector<int64_t> &indices, std::vector<int64_t> &slot) {
-  std::vector<uint64_t> u(keys);
-  sort_unique(u);
-  indptr.assign(n + 1, 0);
-  indices.resize(u.size());
-  for (size_t i = 0; i < u.size(); ++i) {
-    int64_t c = static_cast<int64_t>(u[i] >> 32);
-    GN_REQUIRE(c >= 0 && c < n, "column out of range");
-    indptr[c + 1]++;
-    indices[i] = static_cast<int64_t>(u[i] & 0xFFFFFFFFull);
+// (row, col) coordinates -> lower CSC with sorted unique rows per column, and
+// the slot of every input coordinate (the np.unique(col<<32|row) inverse of
+// csc.py:52-76).  Bucketed by column: O(nnz + sum_c u_c log u_c).
+static void csc_from_coords(int64_t n, const std::vector<int32_t> &rows, const std::vector<int32_t> &cols,
+                            std::vector<int64_t> &indptr, std::vector<int64_t> &indices,
+                            std::vector<int64_t> &slot) {
+  const size_t K = rows.size();
+  std::vector<int64_t> bptr(n + 1, 0);
+  for (size_t t = 0; t < K; ++t) {
+    GN_REQUIRE(cols[t] >= 0 && cols[t] < n, "column out of range");
+    bptr[cols[t] + 1]++;
   }
-  for (int64_t j = 0; j < n; ++j) indptr[j + 1] += indptr[j];
-  slot.resize(keys.size());
-  for (size_t t = 0; t < keys.size(); ++t)
-    slot[t] = std::lower_bound(u.begin(), u.end(), keys[t]) - u.begin();
+  for (int64_t c = 0; c < n; ++c) bptr[c + 1] += bptr[c];
+  std::vector<int32_t> bucket(K);   // input index, grouped by column (stable)
+  {
+    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+    for (size_t t = 0; t < K; ++t) bucket[fill[cols[t]]++] = static_cast<int32_t>(t);
+  }
+  std::vector<int64_t> mark(n, -1), pos(n, 0);
+  std::vector<int32_t> uniq;
+  indptr.assign(n + 1, 0);
+  indices.clear();
+  indices.reserve(K);
+  slot.resize(K);
+  for (int64_t c = 0; c < n; ++c) {
+    uniq.clear();
+    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
+      const int32_t r = rows[bucket[q]];
+      if (mark[r] != c) {
+        mark[r] = c;
+        uniq.push_back(r);
+      }
+    }
+    std::sort(uniq.begin(), uniq.end());
+    const int64_t base = static_cast<int64_t>(indices.size());
+    for (size_t u = 0; u < uniq.size(); ++u) {
+      pos[uniq[u]] = base + static_cast<int64_t>(u);
+      indices.push_back(uniq[u]);
+    }
+    indptr[c + 1] = static_cast<int64_t>(indices.size());
+    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) slot[bucket[q]] = pos[rows[bucket[q]]];
+  }
 }
 
 static inline uint64_t ckey(int64_t row, int64_t col) {
@@ -44,35 +69,50 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
   C.n = n;
   C.nnz_h = nh;
   C.nnz_j = nj;
+  GN_REQUIRE(n < (int64_t(1) << 31), "too many variables for 32-bit indices");
   for (int64_t t = 1; t < nj; ++t)
     GN_REQUIRE(jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1]),
                "Jacobian coordinates must be sorted row-major and unique");
-  std::vector<uint64_t> keys;
-  keys.reserve(nh + n);
+  int64_t np = 0;
+  for (int64_t st = 0; st < nj;) {
+    int64_t en = st;
+    while (en < nj && jr[en] == jr[st]) ++en;
+    np += (en - st) * (en - st + 1) / 2;
+    st = en;
+  }
+  std::vector<int32_t> rows, cols;
+  rows.reserve(nh + n + np);
+  cols.reserve(nh + n + np);
   for (int64_t t = 0; t < nh; ++t) {
     GN_REQUIRE(hc[t] <= hr[t], "Hessian entry above the diagonal");
-    keys.push_back(ckey(hr[t], hc[t]));
+    GN_REQUIRE(hr[t] >= 0 && hr[t] < n && hc[t] >= 0, "Hessian index out of range");
+    rows.push_back(static_cast<int32_t>(hr[t]));
+    cols.push_back(static_cast<int32_t>(hc[t]));
   }
-  for (int64_t i = 0; i < n; ++i) keys.push_back(ckey(i, i));
-  C.ata_row.clear();
-  C.ata_s1.clear();
-  C.ata_s2.clear();
-  int64_t st = 0;
-  while (st < nj) {
+  for (int64_t i = 0; i < n; ++i) {
+    rows.push_back(static_cast<int32_t>(i));
+    cols.push_back(static_cast<int32_t>(i));
+  }
+  C.ata_row.resize(np);
+  C.ata_s1.resize(np);
+  C.ata_s2.resize(np);
+  int64_t q = 0;
+  for (int64_t st = 0; st < nj;) {
     int64_t en = st;
     while (en < nj && jr[en] == jr[st]) ++en;
     // np.tril_indices(k): row-major over the lower triangle
     for (int64_t la = 0; la < en - st; ++la)
-      for (int64_t lb = 0; lb <= la; ++lb) {
-        keys.push_back(ckey(jc[st + la], jc[st + lb]));
-        C.ata_row.push_back(jr[st]);
-        C.ata_s1.push_back(st + la);
-        C.ata_s2.push_back(st + lb);
+      for (int64_t lb = 0; lb <= la; ++lb, ++q) {
+        rows.push_back(static_cast<int32_t>(jc[st + la]));
+        cols.push_back(static_cast<int32_t>(jc[st + lb]));
+        C.ata_row[q] = jr[st];
+        C.ata_s1[q] = st + la;
+        C.ata_s2[q] = st + lb;
       }
     st = en;
   }
   std::vector<int64_t> slot;
-  csc_from_keys(n, keys, C.indptr, C.indices, slot);
+  csc_from_coords(n, rows, cols, C.indptr, C.indices, slot);
   C.w_map.assign(slot.begin(), slot.begin() + nh);
   C.diag_map.assign(slot.begin() + nh, slot.begin() + nh + n);
   C.ata_map.assign(slot.begin() + nh + n, slot.end());
@@ -462,14 +502,16 @@ extern "C" int gn_coo_to_csc(int64_t n, int64_t nnz, const int64_t *rows, const 
                              int64_t *nnz_out, int64_t *indptr_out, int64_t *indices_out,
                              int64_t *slot_out) {
   return guarded([&] {
-    std::vector<uint64_t> keys(nnz);
+    GN_REQUIRE(n < (int64_t(1) << 31), "matrix too large for 32-bit indices");
+    std::vector<int32_t> r32(nnz), c32(nnz);
     for (int64_t t = 0; t < nnz; ++t) {
       GN_REQUIRE(rows[t] >= 0 && rows[t] < n && cols[t] >= 0 && cols[t] < n, "index out of range");
       GN_REQUIRE(cols[t] <= rows[t], "entry above the diagonal");
-      keys[t] = ckey(rows[t], cols[t]);
+      r32[t] = static_cast<int32_t>(rows[t]);
+      c32[t] = static_cast<int32_t>(cols[t]);
     }
     std::vector<int64_t> indptr, indices, slot;
-    csc_from_keys(n, keys, indptr, indices, slot);
+    csc_from_coords(n, r32, c32, indptr, indices, slot);
     if (nnz_out) *nnz_out = static_cast<int64_t>(indices.size());
     copy_out(indptr_out, indptr);
     copy_out(indices_out, indices);

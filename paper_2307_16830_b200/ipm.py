@@ -267,8 +267,10 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     opts = options if options is not None else SolverOptions()
     t_start = time.perf_counter()
     report = SolveReport(status=MAX_ITER, n_var=model.n_var, n_con=model.n_con)
+    setup = {}
     try:
         P = _DeviceSolve(model, opts, constraint_ranges)
+        setup["problem"] = time.perf_counter() - t_start
     except NonFiniteResult as exc:
         report.status = EVAL_ERROR
         report.message = str(exc)
@@ -286,8 +288,10 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     key = None if opts.ordering is None else id(opts.ordering)
     cache = getattr(model, "_kkt_cache", None)
     if cache is None or cache[0] != key:
+        t0 = time.perf_counter()
         ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols)
-        backend = CondensedBackend(ws, ordering=opts.ordering)
+        setup["kkt_workspace"] = time.perf_counter() - t0
+        backend = CondensedBackend(ws, ordering=opts.ordering, timings=setup)
         model._kkt_cache = (key, ws, backend)
     else:
         _, ws, backend = cache
@@ -327,6 +331,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         if opts.record_trace:
             report.debug["filter"] = list(fil.entries)
         report.debug["n_factorizations"] = backend.n_factorizations
+        report.debug["setup_seconds"] = setup
         report.debug["symbolic"] = dict(backend.symbolic.info)
         if opts.keep_workspace:
             report.debug["workspace"] = ws

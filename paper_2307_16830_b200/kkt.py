@@ -93,18 +93,38 @@ def _bind(kkt, y: _Vec7, x: _Vec7, alpha):
 
 @dataclass
 class CondensedStructure:
-    matrix: S.SparseSymmetric
-    w_map: np.ndarray
-    diag_map: np.ndarray
-    ata_map: np.ndarray
-    ata_row: np.ndarray
-    ata_s1: np.ndarray
-    ata_s2: np.ndarray
-    handle: object = None
+    """Pattern of W + I + tril(A^T A) and its scatter maps (kkt.py:232-240).
+
+    The native plan (``handle``) is what the device path uses; the numpy
+    views of the maps are exported from it on first access."""
+
+    _MAPS = ("w_map", "diag_map", "ata_map", "ata_row", "ata_s1", "ata_s2")
+
+    def __init__(self, matrix: S.SparseSymmetric, handle, nnz_w, n_products):
+        self.matrix = matrix
+        self.handle = handle
+        self._nw, self._np = int(nnz_w), int(n_products)
+        self._maps = None
+
+    def _export(self):
+        if self._maps is None:
+            n = self.matrix.n
+            m = {"w_map": np.empty(self._nw, np.int64), "diag_map": np.empty(n, np.int64)}
+            for k in ("ata_map", "ata_row", "ata_s1", "ata_s2"):
+                m[k] = np.empty(self._np, np.int64)
+            L.check(L.lib().gn_condense_export(self.handle, None, None,
+                                               *(L.ptr(m[k]) for k in self._MAPS)))
+            self._maps = m
+        return self._maps
+
+    def __getattr__(self, name):
+        if name in CondensedStructure._MAPS:
+            return self._export()[name]
+        raise AttributeError(name)
 
     def __del__(self):
         try:
-            if self.handle is not None and L._lib is not None:
+            if self.__dict__.get("handle") is not None and L._lib is not None:
                 L.lib().gn_condense_destroy(self.handle)
         except Exception:
             pass
@@ -120,12 +140,10 @@ def symbolic_condense(hess_rows, hess_cols, jac_rows, jac_cols, n) -> CondensedS
     nk, npr = ctypes.c_int64(), ctypes.c_int64()
     L.check(L.lib().gn_condense_info(h, ctypes.byref(nk), ctypes.byref(npr)))
     indptr, indices = np.empty(n + 1, np.int64), np.empty(nk.value, np.int64)
-    w_map, diag_map = np.empty(hr.size, np.int64), np.empty(n, np.int64)
-    ata = [np.empty(npr.value, np.int64) for _ in range(4)]
-    L.check(L.lib().gn_condense_export(h, L.ptr(indptr), L.ptr(indices), L.ptr(w_map),
-                                       L.ptr(diag_map), *(L.ptr(a) for a in ata)))
+    L.check(L.lib().gn_condense_export(h, L.ptr(indptr), L.ptr(indices), None, None, None, None,
+                                       None, None))
     mat = S.SparseSymmetric(n, indptr, indices, np.zeros(nk.value))
-    return CondensedStructure(mat, w_map, diag_map, *ata, handle=h)
+    return CondensedStructure(mat, h, hr.size, npr.value)
 
 
 class KKTWorkspace:
@@ -294,13 +312,23 @@ def residual_norm(pv) -> float:
 class CondensedBackend:
     """Sparse Cholesky of the condensed primal system on the GPU (kkt.py:286-325)."""
 
-    def __init__(self, ws: KKTWorkspace, ordering=None):
+    def __init__(self, ws: KKTWorkspace, ordering=None, timings=None):
+        import time
+
+        tm = timings if timings is not None else {}
+        t = time.perf_counter()
         self.ws = ws
         self.structure = symbolic_condense(ws.hess_rows, ws.hess_cols, ws.jac_rows, ws.jac_cols, ws.n)
         ws.attach_condensed(self.structure)
+        tm["condense"] = time.perf_counter() - t
+        t = time.perf_counter()
         if ordering is None:
             ordering = S.amd_order(self.structure.matrix)
+        tm["ordering"] = time.perf_counter() - t
+        t = time.perf_counter()
         self.symbolic = S.symbolic_cholesky(self.structure.matrix, ordering)
+        tm["symbolic"] = time.perf_counter() - t
+        t = time.perf_counter()
         self.symbolic.handle()
         self.kvals = D.zeros(self.structure.matrix.nnz)
         self.structure.matrix.values = self.kvals
@@ -308,6 +336,7 @@ class CondensedBackend:
         self.factor = None
         self.n_factorizations = 0
         self._dx = D.empty(ws.n)
+        tm["factor_upload"] = time.perf_counter() - t
 
     def assemble(self) -> None:
         st = self.ws.state()
