@@ -9,12 +9,23 @@ class DeviceUnavailable(RuntimeError):
     """Raised when a device entry point runs without a CUDA device."""
 
 
+_available = False
+_devices: dict = {}
+
+
 def require_cuda() -> torch.device:
-    if not torch.cuda.is_available():
-        raise DeviceUnavailable(
-            "the condensed-space solve path runs on the GPU only (no CPU fallback); "
-            "no CUDA device is visible")
-    return torch.device("cuda", torch.cuda.current_device())
+    global _available
+    if not _available:
+        if not torch.cuda.is_available():
+            raise DeviceUnavailable(
+                "the condensed-space solve path runs on the GPU only (no CPU fallback); "
+                "no CUDA device is visible")
+        _available = True
+    i = torch.cuda.current_device()
+    d = _devices.get(i)
+    if d is None:
+        d = _devices[i] = torch.device("cuda", i)
+    return d
 
 
 def stream_ptr(stream=None) -> int:
