@@ -271,6 +271,11 @@ int gn_ipm_direction(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, doub
 /* xt = x + alpha dx, st = s + alpha ds (ipm.py:482-483) */
 int gn_ipm_trial_point(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                        double *xt, double *st, void *stream);
+/* same at alpha = min(alpha_pair[0], alpha_pair[1]) read from the device
+ * (the gn_ipm_direction output), so the first line-search trial needs no
+ * host round trip */
+int gn_ipm_trial_point_at(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                          const double *alpha_pair, double *xt, double *st, void *stream);
 /* scal[0..5) = (theta_t, log-sums of the four trial widths) (ipm.py:490-492);
  * a non-positive finite width yields a NaN log-sum */
 int gn_ipm_trial_merit(gn_kkt *k, const gn_ipm_vecs *v, const double *ct, const double *xt,

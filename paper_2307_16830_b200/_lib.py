@@ -99,6 +99,7 @@ _SIGS = {
     "gn_ipm_direction": (c_i32, [P, P, P, c_dbl, c_dbl, P, P]),
     "gn_ipm_trial_point": (c_i32, [P, P, P, c_dbl, P, P, P]),
     "gn_ipm_trial_merit": (c_i32, [P, P, P, P, P, P, P]),
+    "gn_ipm_trial_point_at": (c_i32, [P, P, P, P, P, P, P]),
     "gn_ipm_accept": (c_i32, [P, P, P, c_dbl, c_dbl, c_dbl, c_dbl, P, P]),
 }
 

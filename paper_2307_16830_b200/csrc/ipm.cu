@@ -163,6 +163,17 @@ __global__ void trial_point_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 
   if (i < m) s_t[i] = v.s[i] + alpha * st.s[i];
 }
 
+// first trial of the line search at alpha_max = min(alpha_x, alpha_s) read
+// from the device (Python's min(a0, a1)), so it needs no host round trip
+__global__ void trial_point_at_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st,
+                                      const double *alpha_pair, double *xt, double *s_t) {
+  const double a0 = alpha_pair[0], a1 = alpha_pair[1];
+  const double alpha = a1 < a0 ? a1 : a0;
+  int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) xt[i] = v.x[i] + alpha * st.x[i];
+  if (i < m) s_t[i] = v.s[i] + alpha * st.s[i];
+}
+
 __global__ void __launch_bounds__(kRedThreads)
 trial_merit_kernel(int64_t n, int64_t m, gn_ipm_vecs v, const double *ct, const double *xt,
                    const double *s_t, RedSpec rs) {
@@ -265,6 +276,14 @@ extern "C" int gn_ipm_trial_point(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7
     GN_LAUNCH(trial_point_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps, alpha,
                                                                                xt, st);
     GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_ipm_trial_point_at(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                     const double *alpha_pair, double *xt, double *st, void *stream) {
+  return guarded([&] {
+    GN_LAUNCH(trial_point_at_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v,
+              *steps, alpha_pair, xt, st);
   });
 }
 

@@ -25,8 +25,8 @@ import torch
 from . import _lib as L
 from . import device as D
 from .autodiff import C, F, GRAD, HESS, JAC, NonFiniteResult, evaluator
-from .kkt import (CondensedBackend, DegenerateInterior, KKTWorkspace, PVec, RegState,
-                  RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
+from .kkt import (CondensedBackend, DegenerateInterior, FactorizationFailed, KKTWorkspace, PVec,
+                  RegState, RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
                   solve_with_regularization)
 from .profiling import span
 
@@ -428,9 +428,21 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), stream))
         t0 = timer.start()
         try:
-            (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg)
+            # speculative: factor with delta_w = delta_c = 0 and solve without
+            # reading the pivot flag; it comes back with the first refinement
+            # read, and only a failure falls back to the regularisation
+            # schedule of solve_with_regularization (kkt.py:424-447)
+            ws.delta_w = ws.delta_c = 0.0
+            backend.factorize_async()
+            dx, ds, dy = backend.solve_pvec(pv)
+            delta_w = 0.0
             steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
-            ir = iterative_refinement(ws, backend, steps, pv)
+            try:
+                ir = iterative_refinement(ws, backend, steps, pv, check_factor=backend.fws.fail)
+            except FactorizationFailed:
+                (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg)
+                steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
+                ir = iterative_refinement(ws, backend, steps, pv)
         except RegularizationExhausted as exc:
             timer.stop("linear", t0)
             return finish(REGULARIZATION_EXHAUSTED, str(exc))
@@ -441,16 +453,22 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         stc = steps.c_struct()
         L.check(lib.gn_ipm_direction(ws.handle, ctypes.byref(V), ctypes.byref(stc), mu, tau,
                                      L.ptr(P.scal[50:54]), stream))
-        d, _, _ = P.read(50, 54)
-        alpha_max = min(float(d[0]), float(d[1]))
-        alpha_z, dphi = float(d[2]), float(d[3])
-        # ---- filter line search (ipm.py:478-519)
-        alpha = alpha_max
+        # ---- filter line search (ipm.py:478-519); the first trial runs at
+        # alpha_max read on the device and returns with the direction scalars
+        alpha = alpha_z = dphi = 0.0
         accepted = f_type = False
         theta_t = phi_t = np.nan
-        while alpha >= opts.alpha_min:
-            L.check(lib.gn_ipm_trial_point(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha,
-                                           L.ptr(P.xt), L.ptr(P.st), stream))
+        first = True
+        while True:
+            if first:
+                L.check(lib.gn_ipm_trial_point_at(ws.handle, ctypes.byref(V), ctypes.byref(stc),
+                                                  L.ptr(P.scal[50:52]), L.ptr(P.xt), L.ptr(P.st),
+                                                  stream))
+            else:
+                if alpha < opts.alpha_min:
+                    break
+                L.check(lib.gn_ipm_trial_point(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha,
+                                               L.ptr(P.xt), L.ptr(P.st), stream))
             ev_flags.zero_()
             t0 = timer.start()
             with span("ad_trial"):
@@ -461,6 +479,12 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
                                            L.ptr(P.st), L.ptr(P.scal[54:59]), stream))
             P.flags[0:1].copy_(ev_flags)
             tv, adf, _ = P.read(49, 59)
+            if first:
+                first = False
+                alpha = min(float(tv[1]), float(tv[2]))
+                alpha_z, dphi = float(tv[3]), float(tv[4])
+                if alpha < opts.alpha_min:
+                    break
             if adf:
                 alpha *= 0.5
                 continue

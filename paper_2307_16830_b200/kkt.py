@@ -415,15 +415,26 @@ class RefinementStats:
         return self.final_residual / self.scale
 
 
-def iterative_refinement(ws, backend, steps: Steps, pv: PVec) -> RefinementStats:
+class FactorizationFailed(RuntimeError):
+    """Raised by iterative_refinement(check_factor=...) when the speculative
+    factorisation behind ``steps`` was not positive definite."""
+
+
+def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None) -> RefinementStats:
     """Refine against the full seven-block system in place (kkt.py:467-491).
 
-    The matrix scale and the first residual norm come back in one read.
+    The matrix scale and the first residual norm come back in one read;
+    ``check_factor`` (the device failing-pivot word of a factorisation whose
+    success was not checked yet) rides along in the same read.
     """
     scal = ws._scal
     ws.matrix_scale_device(scal[2:3])
     res = ws.residual_full(steps, pv, norm_out=scal[0:2])
-    host = scal[0:3].cpu().numpy()
+    if check_factor is not None:
+        scal[3:4].copy_(check_factor)
+    host = scal[0:4].cpu().numpy()
+    if check_factor is not None and host[3] < ws.n:
+        raise FactorizationFailed("condensed matrix not positive definite")
     scale, rnorm = float(host[2]), float(host[0])
     target = KAPPA_IR * np.finfo(float).eps * scale
     stats = RefinementStats(initial_residual=rnorm, final_residual=rnorm, scale=scale)
