@@ -44,7 +44,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
 METRIC = "ACOPF solve time (s) + per-iter AD/condense/refactor ms, 10k–78k-bus grids"
-WORKLOADS = {"C3": 714, "C2": 143, "C4": 5606, "C1": 1}
+WORKLOADS = {"C3": 714, "C2": 143, "C4": 5606, "C1": 1, "C5": 97}
 
 
 def _peaks():
@@ -165,6 +165,134 @@ def run_reference(args):
     return 0
 
 
+def _c5_worker(seed):
+    """One C5 instance by the oracle port (reference arm; one process per core)."""
+    dt, rep = cpu_baseline_instance(WORKLOADS["C5"], seed, 1e-6)
+    return dt, rep.status, rep.iterations
+
+
+def cpu_baseline_instance(tiles, seed, tol):
+    from oracle import ipm as OI
+    from oracle import model as OM
+    from paper_2307_16830_b200 import kkt, sparse
+    from paper_2307_16830_b200.acopf import build_acopf
+    from paper_2307_16830_b200.grids import tiled_case
+    from paper_2307_16830_b200.matpower import parse_matpower
+
+    am = build_acopf(parse_matpower(tiled_case(tiles, seed=seed)))
+    m = am.model
+    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
+    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
+    perm = sparse.amd_order(cs.matrix)
+    t = time.perf_counter()
+    rep = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol), am.ranges, ordering=perm)
+    return time.perf_counter() - t, rep
+
+
+def run_batch_reference(args):
+    """--impl reference --workload C5: the oracle port on all host cores, one
+    instance per process (the reference's run_suite(parallel=P) shape,
+    src/bench.py:166-176), on a bounded sample of the batch; the batch time
+    is projected linearly from the sample (stated in cpu_baseline.sample)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from concurrent.futures import ProcessPoolExecutor
+
+    cores = len(os.sched_getaffinity(0))
+    sample = min(args.batch, max(cores, 2))
+    times = []
+    with ProcessPoolExecutor(cores) as ex:
+        list(ex.map(_c5_worker, [10_000 + i for i in range(min(cores, 2))]))   # warm-up
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            res = list(ex.map(_c5_worker, range(sample)))
+            times.append((time.perf_counter() - t) * args.batch / sample)
+    v = float(np.mean(times))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": 1, "ms_per_step": 1e3 * v, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5: batch of {args.batch} load-perturbed 1,358-bus instances, tol 1e-6"},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} instances solved in parallel on {cores} processes per step, "
+                                   f"projected to {args.batch} (ordering injected, loop-fair)"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "statuses": sorted({r[1] for r in res}),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_batch(args):
+    """--workload C5: B load-perturbed 1,358-bus instances partitioned over
+    the ranks (contiguous blocks), one shared symbolic plan per rank, one
+    final gather (NCCL) of fixed-size result records.  A step = the whole
+    batch; value = max over ranks of the step time."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2307_16830_b200 import SolverOptions, _lib
+    from paper_2307_16830_b200 import batch as BT
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mine = BT.partition(args.batch, world, rank)
+    inst = BT.perturbed_instances(WORKLOADS["C5"], list(mine))
+    n_var = inst[0].model.n_var
+    opts = SolverOptions(tol=args.tol)
+    clocks = _clock_sampler() if rank == 0 else None
+    time.sleep(1.0)
+    for _ in range(max(1, args.warmup)):
+        BT.solve_batch(inst[:2], opts)
+    _lib.stats(reset=True)
+    times = []
+    full = None
+    for _ in range(args.steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        reps = BT.solve_batch(inst, opts)
+        rec = BT.pack_records(reps, n_var)
+        full = BT.gather_records(rec, args.batch, world, rank,
+                                 device=torch.device("cuda", local)) if world > 1 else rec
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    launches, _ = _lib.stats(reset=True)
+    clk = _clock_summary(clocks, local) if rank == 0 else None
+    tt = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    v = float(tt.item())
+    stat = [BT.unpack_record(r, n_var)["status"] for r in full]
+    its = [BT.unpack_record(r, n_var)["iterations"] for r in full]
+    line = {
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * v, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md Appendix B, loads x (1+U(-0.1,0.1)), seed = instance index)",
+        "config": {"workload": f"C5: batch of {args.batch} load-perturbed 1,358-bus instances "
+                               f"({n_var} vars each), tol {args.tol:g}",
+                   "parallelism": f"instances partitioned over {world} GPU(s), one final gather"},
+        "instances_per_s": args.batch / v,
+        "optimal": int(sum(s == "optimal" for s in stat)), "mean_iterations": float(np.mean(its)),
+        "e2e": None, "clocks": clk, "gpu_launches": launches,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -175,7 +303,10 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--batch", type=int, default=256, help="C5: number of instances")
     args = ap.parse_args()
+    if args.workload == "C5":
+        return run_batch_reference(args) if args.impl == "reference" else run_batch(args)
     if args.impl == "reference":
         return run_reference(args)
 
