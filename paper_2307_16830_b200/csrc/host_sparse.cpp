@@ -448,6 +448,23 @@ static void front_plan(Symbolic &S) {
     for (int64_t l = 0; l < 2 * S.n_levels; ++l) lc[l + 1] += lc[l];
     for (int64_t J = 0; J < nf; ++J) S.order[lc[bucket(J)]++] = static_cast<int32_t>(J);
   }
+  // top fronts: the highest complete levels of the large part holding at
+  // most kTopFronts fronts, all of them tall (the cluster kernel's share)
+  S.nf_top = 0;
+  {
+    int64_t k = nf, lev = -1;
+    while (k > S.nf_small) {
+      const int64_t l = S.level[S.order[k - 1]];
+      int64_t b = k;
+      while (b > S.nf_small && S.level[S.order[b - 1]] == l) --b;
+      bool tall = true;
+      for (int64_t q = b; q < k; ++q) tall = tall && S.f_nrows[S.order[q]] >= kTopMinRows;
+      if (!tall || nf - b > kTopFronts) break;
+      k = b;
+      lev = l;
+    }
+    S.nf_top = lev >= 0 ? nf - k : 0;
+  }
 }
 
 }  // namespace gn

@@ -128,6 +128,8 @@ struct Condense {
 
 // ------------------------------------------------------- symbolic factor
 constexpr int kWarpFrontRows = 32;   // fronts this small are factored by one warp
+constexpr int kTopFronts = 24;       // at most this many top fronts go to the cluster kernel
+constexpr int kTopMinRows = 96;      // ... and only fronts at least this tall
 
 // device record of one front (loaded with four 16-byte loads)
 struct alignas(16) FrontMeta {
@@ -157,6 +159,7 @@ struct Symbolic {
   std::vector<int64_t> a_kslot, a_fpos;        // (kvals slot, F offset)
   std::vector<int32_t> order;                  // task order: [small by level | large by level]
   int64_t nf_small = 0;                        // warp-task fronts (prefix of order)
+  int64_t nf_top = 0;                          // cluster-task fronts (suffix of order)
   std::vector<int32_t> level;
   std::vector<int64_t> l_export;               // reference L slot -> F offset
   int64_t dinv_off = 0;   // fronts buffer: [fronts | inverse diagonal (n)]
