@@ -135,7 +135,15 @@ void gn_symbolic_destroy(gn_symbolic *sym);
 #define GN_AD_JAC 8u
 #define GN_AD_HESS 16u
 
+/* Uploads the plan and compiles one straight-line device function per
+ * distinct pattern tape (NVRTC, sm_100a, cached per process); without NVRTC
+ * (or with GN_AD_INTERPRETER=1) a generic tape-interpreter kernel is used. */
 int gn_model_upload(gn_model *mdl);
+/* the generated CUDA source of the pattern kernels (host only; two-phase:
+ * *needed = bytes incl. the terminator) */
+int gn_model_pattern_source(const gn_model *mdl, char *buf, size_t len, size_t *needed);
+/* "patterns" or "interpreter: <reason>" */
+int gn_model_ad_backend(const gn_model *mdl, char *buf, size_t len);
 /* free the device copy of the plan (the host structure stays valid) */
 int gn_model_release(gn_model *mdl);
 /* Objective, constraints, gradient, Jacobian and Lagrangian Hessian values.

@@ -107,3 +107,25 @@ def eval_lagrangian_hessian(model: CompiledModel, x, y, obj_weight: float = 1.0,
     if y is None or (not D.is_tensor(y) and np.asarray(y).size == 0):
         y = np.zeros(max(1, model.n_con))
     return _run(model, x, HESS, model.nnz_hess, y=y, obj_weight=obj_weight, out=out)
+
+
+def pattern_source(model: CompiledModel) -> str:
+    """CUDA source generated from the model's pattern tapes (one device
+    function per distinct pattern; compiled with NVRTC at upload)."""
+    import ctypes
+
+    need = ctypes.c_size_t()
+    L.check(L.lib().gn_model_pattern_source(model._handle, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    L.check(L.lib().gn_model_pattern_source(model._handle, buf, need.value, None))
+    return buf.value.decode()
+
+
+def ad_backend(model: CompiledModel) -> str:
+    """'patterns' (generated kernels) or 'interpreter: <reason>'."""
+    import ctypes
+
+    model.device_plan()
+    buf = ctypes.create_string_buffer(512)
+    L.check(L.lib().gn_model_ad_backend(model._handle, buf, 512))
+    return buf.value.decode()

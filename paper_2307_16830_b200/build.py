@@ -64,7 +64,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if failed:
         raise RuntimeError("libgridopf build failed")
     tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"])
+    # libnvrtc / libcuda are dlopen'ed at run time (ad_codegen.cpp)
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -12,6 +12,10 @@
 // A single-CTA kernel reduces the objective.
 #include <cmath>
 
+#include <cstdio>
+#include <cstdlib>
+
+#include "ad_codegen.h"
 #include "device.cuh"
 
 namespace gn {
@@ -326,6 +330,9 @@ static void release_model(Model &M) {
                 M.d.c_ptr, M.d.grad_ptr, M.d.jac_ptr, M.d.hess_ptr, M.d.c_src, M.d.grad_src,
                 M.d.jac_src, M.d.hess_src, M.d.obj_src, M.d.jac_rows, M.d.obj_block_ptr};
   for (void *p : ps) dev_free(p);
+  dev_free(M.d_genblk);
+  M.d_genblk = nullptr;
+  M.pattern_fn = nullptr;
   M.d = Model::Dev{};
   M.uploaded = false;
 }
@@ -403,6 +410,24 @@ static void upload_model(Model &M) {
   M.d.obj_block_ptr = dev_upload(M.obj_block_ptr);
   M.d.n_obj_blocks = static_cast<int32_t>(M.obj_block_ptr.size()) - 1;
   M.d.jac_rows = dev_upload(narrow<int32_t>(M.jac_rows));
+  // pattern kernels generated from the tapes (NVRTC, cached per source)
+  M.pattern_fn = nullptr;
+  const char *env = std::getenv("GN_AD_INTERPRETER");
+  if (!(env && env[0] == '1') && !db.empty()) {
+    std::vector<int> pat;
+    const std::string src = pattern_source(M, pat);
+    M.pattern_fn = compile_patterns(src, M.pattern_error);
+    if (M.pattern_fn) {
+      struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off; int pattern, pad; };
+      std::vector<GenBlk> gb(db.size());
+      for (size_t b = 0; b < db.size(); ++b)
+        gb[b] = {db[b].cta_begin, db[b].R, db[b].var_off, db[b].par_off, db[b].tgt_off, db[b].contrib_off,
+                 pat[b], 0};
+      M.d_genblk = dev_upload(gb);
+    }
+  } else {
+    M.pattern_error = "disabled by GN_AD_INTERPRETER=1";
+  }
   M.uploaded = true;
 }
 
@@ -411,11 +436,22 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
                     uint32_t what, double *contrib, int32_t *flags, cudaStream_t st) {
   GN_REQUIRE(M.uploaded, "model not uploaded to the device");
   if (what & GN_AD_HESS) GN_REQUIRE(y != nullptr || M.m == 0, "Hessian needs multipliers");
-  if (M.n_ctas_rec > 0)
-    GN_LAUNCH(ad_records_kernel, static_cast<unsigned>(M.n_ctas_rec), kRecThreads, 0, st, 
+  if (M.n_ctas_rec > 0 && M.pattern_fn) {
+    int nblk = static_cast<int>(M.dblocks.size());
+    const void *blk = M.d_genblk;
+    const int32_t *vi = M.d.var_idx, *tg = M.d.targets;
+    const double *pa = M.d.params;
+    unsigned w = what;
+    void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib};
+    GN_REQUIRE(launch_patterns(M.pattern_fn, static_cast<unsigned>(M.n_ctas_rec), st, args),
+               "pattern kernel launch failed");
+    count_launch();
+  } else if (M.n_ctas_rec > 0) {
+    GN_LAUNCH(ad_records_kernel, static_cast<unsigned>(M.n_ctas_rec), kRecThreads, 0, st,
         M.d.blocks, static_cast<int>(M.dblocks.size()), reinterpret_cast<const int4 *>(M.d.tape),
         M.d.consts, M.d.slots, M.d.var_idx, M.d.params, M.d.targets, x, y, con_scale, obj_w, what,
         contrib);
+  }
   GN_LAUNCH_CHECK();
   GatherArgs ga{};
   int ns = 0;
@@ -458,6 +494,24 @@ using namespace gn;
 extern "C" int gn_model_upload(gn_model *M) {
   return guarded([&] {
     if (!M->uploaded) upload_model(*M);
+  });
+}
+
+extern "C" int gn_model_pattern_source(const gn_model *M, char *buf, size_t len, size_t *needed) {
+  return guarded([&] {
+    std::vector<int> pat;
+    const std::string src = pattern_source(*M, pat);
+    if (needed) *needed = src.size() + 1;
+    if (buf && len) std::snprintf(buf, len, "%s", src.c_str());
+  });
+}
+
+extern "C" int gn_model_ad_backend(const gn_model *M, char *buf, size_t len) {
+  return guarded([&] {
+    std::string s = M->pattern_fn ? "patterns" : ("interpreter: " + M->pattern_error);
+    if (buf && len) {
+      std::snprintf(buf, len, "%s", s.c_str());
+    }
   });
 }
 

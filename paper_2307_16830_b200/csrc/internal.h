@@ -101,6 +101,9 @@ struct Model {
   bool uploaded = false;
   std::vector<DevBlock> dblocks;
   int64_t n_ctas_rec = 0;
+  void *pattern_fn = nullptr;        // NVRTC-compiled pattern kernel (nullptr: interpreter)
+  void *d_genblk = nullptr;          // its per-block table (device)
+  std::string pattern_error;         // why the interpreter is used, if it is
   struct Dev {
     DevBlock *blocks = nullptr;
     int32_t *tape = nullptr;  // int4-packed (op, a, b, 0)

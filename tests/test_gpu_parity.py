@@ -359,3 +359,35 @@ def test_end_to_end_matches_oracle_trace_closely(golden_models):
     for a, b in zip(rep.trace, orep.trace):
         assert a[1] == pytest.approx(b[1], rel=1e-5)   # objective per iteration
         assert a[4] == b[4]                              # same barrier sequence
+
+
+def test_generated_pattern_kernels_match_interpreter():
+    """The NVRTC pattern kernels (one straight-line function per pattern tape)
+    against the generic tape interpreter and the oracle, on C1 and case118."""
+    import os
+
+    for tag in ("C1", "T4"):
+        tiles = {"C1": 1, "T4": 4}[tag]
+        outs = {}
+        for mode in ("interp", "patterns"):
+            if mode == "interp":
+                os.environ["GN_AD_INTERPRETER"] = "1"
+            m = build_acopf(parse_matpower(tiled_case(tiles))).model
+            try:
+                backend = ad.ad_backend(m)
+            finally:
+                os.environ.pop("GN_AD_INTERPRETER", None)
+            assert backend.startswith("patterns" if mode == "patterns" else "interpreter"), backend
+            rng = np.random.default_rng(3)
+            x = m.start + 0.01 * rng.standard_normal(m.n_var)
+            yv = rng.standard_normal(m.n_con)
+            outs[mode] = (ad.eval_objective(m, x), ad.eval_constraints(m, x), ad.eval_gradient(m, x),
+                          ad.eval_jacobian(m, x), ad.eval_lagrangian_hessian(m, x, yv, 0.7))
+        om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
+        ref = (OM.objective(om, x), OM.constraints(om, x), OM.gradient(om, x), OM.jacobian(om, x),
+               OM.hessian(om, x, yv, 0.7))
+        for a, b, r in zip(outs["patterns"], outs["interp"], ref):
+            a, b, r = np.atleast_1d(a), np.atleast_1d(b), np.atleast_1d(r)
+            scale = max(1.0, np.max(np.abs(r)))
+            assert np.max(np.abs(a - b)) <= 1e-14 * scale
+            assert np.max(np.abs(a - r)) <= 1e-12 * scale
