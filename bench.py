@@ -434,6 +434,26 @@ def main():
     ref = phases.get("refactor", {"mean_ms": float("nan"), "count": 0})
     achieved = alg_bytes / (ref["mean_ms"] * 1e-3) / 1e9 if ref["count"] else None
     per_iter = {k: v["total_ms"] / (args.steps * max(1, iters)) for k, v in phases.items()}
+    # secondary rooflines: AD (full evaluation) and the condensed assembly
+    import ctypes as _ct
+
+    def _bytes(fn, *a):
+        b = _ct.c_int64()
+        _lib.check(fn(*a, _ct.byref(b)))
+        return int(b.value)
+
+    secondary = {}
+    for name, span_name, nbytes in (
+            ("ad_full (gn_ad_eval: pattern kernels + gather)", "ad_full",
+             _bytes(_lib.lib().gn_model_traffic, model.device_plan(), 31)),
+            ("assemble (gn_kkt_assemble)", "assemble",
+             _bytes(_lib.lib().gn_kkt_assembly_traffic, ws.handle))):
+        ph = phases.get(span_name)
+        if ph and ph["count"]:
+            ach = nbytes / (ph["mean_ms"] * 1e-3) / 1e9
+            secondary[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                               "frac": ach / peak, "alg_bytes_per_launch": nbytes,
+                               "mean_launch_ms": ph["mean_ms"]}
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -464,6 +484,7 @@ def main():
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": None, "alg_bytes_per_launch": alg_bytes,
                      "mean_launch_ms": ref["mean_ms"]},
+        "rooflines_secondary": secondary,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "e2e_with_ordering": e2e_full,

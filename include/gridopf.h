@@ -142,6 +142,9 @@ int gn_model_upload(gn_model *mdl);
 /* the generated CUDA source of the pattern kernels (host only; two-phase:
  * *needed = bytes incl. the terminator) */
 int gn_model_pattern_source(const gn_model *mdl, char *buf, size_t len, size_t *needed);
+/* compulsory HBM bytes of one gn_ad_eval with this what-mask: inputs once,
+ * index maps once, outputs once (the roofline numerator) */
+int gn_model_traffic(const gn_model *mdl, uint32_t what, int64_t *bytes);
 /* "patterns" or "interpreter: <reason>" */
 int gn_model_ad_backend(const gn_model *mdl, char *buf, size_t len);
 /* free the device copy of the plan (the host structure stays valid) */
@@ -211,6 +214,8 @@ int gn_kkt_matvec(gn_kkt *k, int kind, const double *vals, const double *v, doub
 /* K = W + (Sigma_x + dw) I + A^T D A in the condensed CSC layout
  * (CondensedBackend.assemble, kkt.py:300-312) */
 int gn_kkt_assemble(gn_kkt *k, const gn_kkt_state *st, double *kvals, void *stream);
+/* compulsory HBM bytes of one gn_kkt_assemble (roofline numerator) */
+int gn_kkt_assembly_traffic(const gn_kkt *k, int64_t *bytes);
 /* (qx, qs, qy) = condense_pvec(pv); rhs = qx + A^T (C qs + D qy)
  * (kkt.py:159-167) */
 int gn_kkt_condense_rhs(gn_kkt *k, const gn_kkt_state *st, const gn_vec7 *pv, double *qx,

@@ -76,6 +76,8 @@ _SIGS = {
     "gn_symbolic_destroy": (None, [P]),
     "gn_model_upload": (c_i32, [P]),
     "gn_model_release": (c_i32, [P]),
+    "gn_model_traffic": (c_i32, [P, c_u32, P]),
+    "gn_kkt_assembly_traffic": (c_i32, [P, P]),
     "gn_model_ad_backend": (c_i32, [P, ctypes.c_char_p, ctypes.c_size_t]),
     "gn_model_pattern_source": (c_i32, [P, ctypes.c_char_p, ctypes.c_size_t, P]),
     "gn_ad_eval": (c_i32, [P, P, P, c_dbl, P, c_dbl, P, P, P, P, P, c_u32, P, P, P]),

@@ -506,6 +506,27 @@ extern "C" int gn_model_pattern_source(const gn_model *M, char *buf, size_t len,
   });
 }
 
+extern "C" int gn_model_traffic(const gn_model *M, uint32_t what, int64_t *bytes) {
+  return guarded([&] {
+    const Model &m = *M;
+    int64_t b = 8 * m.n;                                    // x
+    if (what & GN_AD_HESS) b += 8 * m.m;                    // y
+    if (what & (GN_AD_C | GN_AD_JAC | GN_AD_HESS)) b += 8 * m.m;   // con_scale
+    for (const auto &blk : m.blocks)                        // record data (SoA)
+      b += blk.R * (4 * blk.nv + 8 * blk.np + (blk.kind != 0 ? 4 : 0));
+    auto gather = [&](const std::vector<int64_t> &ptr, const std::vector<int64_t> &src, int64_t out) {
+      return static_cast<int64_t>(8 * ptr.size() + 4 * src.size() + 8 * out);
+    };
+    if (what & GN_AD_C) b += gather(m.c_ptr, m.c_src, m.m);
+    if (what & GN_AD_GRAD) b += gather(m.grad_ptr, m.grad_src, m.n);
+    if (what & GN_AD_JAC) b += gather(m.jac_ptr, m.jac_src, static_cast<int64_t>(m.jac_rows.size())) +
+                               4 * static_cast<int64_t>(m.jac_rows.size());
+    if (what & GN_AD_HESS) b += gather(m.hess_ptr, m.hess_src, static_cast<int64_t>(m.hess_rows.size()));
+    if (what & GN_AD_F) b += 4 * static_cast<int64_t>(m.obj_src.size()) + 8;
+    *bytes = b;
+  });
+}
+
 extern "C" int gn_model_ad_backend(const gn_model *M, char *buf, size_t len) {
   return guarded([&] {
     std::string s = M->pattern_fn ? "patterns" : ("interpreter: " + M->pattern_error);

@@ -191,7 +191,7 @@ struct Symbolic {
 
 // ---------------------------------------------------------- KKT gathers
 struct Kkt {
-  int64_t n = 0, m = 0, nh = 0, nj = 0, nk = 0;
+  int64_t n = 0, m = 0, nh = 0, nj = 0, nk = 0, np = 0;
   bool has_assembly = false;
   struct Dev {
     int64_t *a_rowptr = nullptr;   // A by rows (jac order)
@@ -200,12 +200,13 @@ struct Kkt {
     int32_t *at_p = nullptr, *at_row = nullptr;
     int64_t *w_ptr = nullptr;      // symmetric W per row: hess positions + partner
     int32_t *w_p = nullptr, *w_j = nullptr;
-    int64_t *k_ptr = nullptr;      // assembly: per K slot products (row, s1, s2)
+    int32_t *k_ptr = nullptr;      // assembly: per K slot products (row, s1, s2)
     int32_t *k_row = nullptr, *k_s1 = nullptr, *k_s2 = nullptr;
     int32_t *k_w = nullptr, *k_diag = nullptr;
     double *partials = nullptr;
     unsigned int *counter = nullptr;
     double *scratch = nullptr;     // m doubles
+    double *dvec = nullptr;        // D per row (assembly)
   } d;
   ~Kkt();
 };

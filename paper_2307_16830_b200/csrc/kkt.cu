@@ -15,7 +15,7 @@ namespace gn {
 Kkt::~Kkt() {
   void *ps[] = {d.a_rowptr, d.a_col, d.at_ptr, d.at_p, d.at_row, d.w_ptr, d.w_p, d.w_j,
                 d.k_ptr, d.k_row, d.k_s1, d.k_s2, d.k_w, d.k_diag, d.partials, d.counter,
-                d.scratch};
+                d.scratch, d.dvec};
   for (void *p : ps) dev_free(p);
 }
 
@@ -95,25 +95,52 @@ __global__ void at_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *p
   out[j] = acc;
 }
 
+// D = (Sigma_s + dw) C, C = 1 / (dc Sigma_s + (1 + dc dw)) per row
+// (kkt.py:153-157), once per row instead of once per product
+__global__ void d_rows_kernel(int64_t m, gn_kkt_state st, double *d) {
+  int64_t r = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  if (r >= m) return;
+  const double ssr = st.ss[r];
+  const double cfac = __dadd_rn(1.0, __dmul_rn(st.dc, st.dw));
+  const double c = 1.0 / __dadd_rn(__dmul_rn(st.dc, ssr), cfac);
+  d[r] = __dmul_rn(__dadd_rn(ssr, st.dw), c);
+}
+
 // K[slot] = ((0 + W) + (sigma_x + dw)) + sum (d[row] * a[s1]) * a[s2] in
-// product order (kkt.py:300-312); no FMA contraction.
-__global__ void assemble_kernel(int64_t nk, const int64_t *kp, const int32_t *krow, const int32_t *ks1,
-                                const int32_t *ks2, const int32_t *kw, const int32_t *kd,
-                                gn_kkt_state st, double *K) {
+// product order (kkt.py:300-312); no FMA contraction, so the values are
+// bitwise the reference's.  One thread per K slot; the indices of up to four
+// products are loaded before their values (memory-level parallelism).
+__global__ void __launch_bounds__(kT)
+assemble_kernel(int64_t nk, const int32_t *__restrict__ kp, const int32_t *__restrict__ krow,
+                const int32_t *__restrict__ ks1, const int32_t *__restrict__ ks2,
+                const int32_t *__restrict__ kw, const int32_t *__restrict__ kd, gn_kkt_state st,
+                const double *__restrict__ d, double *K) {
   int64_t s = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (s >= nk) return;
+  const int p0 = __ldg(kp + s), p1 = __ldg(kp + s + 1);
+  const int w = __ldg(kw + s), dg = __ldg(kd + s);
   double acc = 0.0;
-  int w = kw[s];
-  if (w >= 0) acc = __dadd_rn(acc, st.w[w]);
-  int dg = kd[s];
-  if (dg >= 0) acc = __dadd_rn(acc, __dadd_rn(st.sx[dg], st.dw));
-  const double cfac = __dadd_rn(1.0, __dmul_rn(st.dc, st.dw));
-  for (int64_t p = kp[s]; p < kp[s + 1]; ++p) {
-    const int r = krow[p];
-    const double ssr = st.ss[r];
-    const double c = 1.0 / __dadd_rn(__dmul_rn(st.dc, ssr), cfac);
-    const double d = __dmul_rn(__dadd_rn(ssr, st.dw), c);
-    acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(d, st.a[ks1[p]]), st.a[ks2[p]]));
+  if (w >= 0) acc = __dadd_rn(acc, __ldg(st.w + w));
+  if (dg >= 0) acc = __dadd_rn(acc, __dadd_rn(__ldg(st.sx + dg), st.dw));
+  for (int p = p0; p < p1; p += 4) {
+    int r[4], a1[4], a2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = p + u < p1;
+      r[u] = ok ? __ldg(krow + p + u) : 0;
+      a1[u] = ok ? __ldg(ks1 + p + u) : 0;
+      a2[u] = ok ? __ldg(ks2 + p + u) : 0;
+    }
+    double dv[4], v1[4], v2[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      dv[u] = __ldg(d + r[u]);
+      v1[u] = __ldg(st.a + a1[u]);
+      v2[u] = __ldg(st.a + a2[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p + u < p1) acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(dv[u], v1[u]), v2[u]));
   }
   K[s] = acc;
 }
@@ -356,22 +383,25 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
   K.d.counter = dev_alloc<unsigned int>(1);
   GN_CUDA(cudaMemset(K.d.counter, 0, sizeof(unsigned int)));
   K.d.scratch = dev_alloc<double>(m > 0 ? m : 1);
+  K.d.dvec = dev_alloc<double>(m > 0 ? m : 1);
   if (cs) {
     GN_REQUIRE(cs->n == n && cs->nnz_h == nh && cs->nnz_j == nj, "condensed structure mismatch");
     const int64_t nk = static_cast<int64_t>(cs->indices.size());
     const int64_t np = static_cast<int64_t>(cs->ata_map.size());
     K.nk = nk;
+    K.np = np;
     std::vector<int32_t> kw(nk, -1), kd(nk, -1);
     for (int64_t p = 0; p < nh; ++p) {
       GN_REQUIRE(kw[cs->w_map[p]] == -1, "duplicate W entry in a K slot");
       kw[cs->w_map[p]] = static_cast<int32_t>(p);
     }
     for (int64_t i = 0; i < n; ++i) kd[cs->diag_map[i]] = static_cast<int32_t>(i);
-    std::vector<int64_t> kp(nk + 1, 0);
+    GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
+    std::vector<int32_t> kp(nk + 1, 0);
     for (int64_t p = 0; p < np; ++p) kp[cs->ata_map[p] + 1]++;
     for (int64_t s = 0; s < nk; ++s) kp[s + 1] += kp[s];
     std::vector<int32_t> krow(np), k1(np), k2(np);
-    std::vector<int64_t> fl(kp.begin(), kp.end() - 1);
+    std::vector<int32_t> fl(kp.begin(), kp.end() - 1);
     for (int64_t p = 0; p < np; ++p) {
       int64_t q = fl[cs->ata_map[p]]++;
       krow[q] = static_cast<int32_t>(cs->ata_row[p]);
@@ -437,9 +467,19 @@ extern "C" int gn_kkt_assemble(gn_kkt *K, const gn_kkt_state *st, double *kvals,
   return guarded([&] {
     GN_REQUIRE(K->has_assembly, "KKT plan built without the condensed structure");
     if (K->nk == 0) return;
-    GN_LAUNCH(assemble_kernel, blocks_for(K->nk), kT, 0, ST(stream), K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1, K->d.k_s2,
-                                                            K->d.k_w, K->d.k_diag, *st, kvals);
+    if (K->m) GN_LAUNCH(d_rows_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, *st, K->d.dvec);
+    GN_LAUNCH(assemble_kernel, blocks_for(K->nk), kT, 0, ST(stream), K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1,
+              K->d.k_s2, K->d.k_w, K->d.k_diag, *st, K->d.dvec, kvals);
     GN_LAUNCH_CHECK();
+  });
+}
+
+extern "C" int gn_kkt_assembly_traffic(const gn_kkt *K, int64_t *bytes) {
+  return guarded([&] {
+    GN_REQUIRE(K->has_assembly, "KKT plan built without the condensed structure");
+    // index maps (kp, row/s1/s2, W and diagonal sources), inputs (A, W,
+    // Sigma_x, Sigma_s; D written and read once), output K
+    *bytes = 4 * (K->nk + 1) + 12 * K->np + 8 * K->nk + 8 * (K->nj + K->nh + K->n) + 8 * K->m * 3 + 8 * K->nk;
   });
 }
 
