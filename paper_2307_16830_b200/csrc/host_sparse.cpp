@@ -446,6 +446,11 @@ static void front_plan(Symbolic &S) {
     auto bucket = [&](int64_t J) { return (small[J] ? 0 : S.n_levels) + S.level[J]; };
     for (int64_t J = 0; J < nf; ++J) lc[bucket(J) + 1]++, S.nf_small += small[J];
     for (int64_t l = 0; l < 2 * S.n_levels; ++l) lc[l + 1] += lc[l];
+    // level boundaries of the small part (warp kernels run level by level)
+    S.small_lptr.assign(S.n_levels + 1, 0);
+    for (int64_t l = 0; l < S.n_levels; ++l) S.small_lptr[l + 1] = static_cast<int32_t>(lc[l + 1]);
+    while (S.small_lptr.size() > 1 && S.small_lptr[S.small_lptr.size() - 2] == S.small_lptr.back())
+      S.small_lptr.pop_back();
     for (int64_t J = 0; J < nf; ++J) S.order[lc[bucket(J)]++] = static_cast<int32_t>(J);
   }
   // top fronts: the highest complete levels of the large part holding at

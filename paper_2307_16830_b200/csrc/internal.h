@@ -163,6 +163,7 @@ struct Symbolic {
   std::vector<int32_t> order;                  // task order: [small by level | large by level]
   int64_t nf_small = 0;                        // warp-task fronts (prefix of order)
   int64_t nf_top = 0;                          // cluster-task fronts (suffix of order)
+  std::vector<int32_t> small_lptr;             // level boundaries within order[0, nf_small)
   std::vector<int32_t> level;
   std::vector<int64_t> l_export;               // reference L slot -> F offset
   int64_t dinv_off = 0;   // fronts buffer: [fronts | inverse diagonal (n)]
@@ -181,7 +182,9 @@ struct Symbolic {
     int32_t *a_kslot = nullptr;
     int32_t *a_loc = nullptr;
     int32_t *order = nullptr;
-    int32_t *nchild = nullptr;        // template counters
+    int32_t *nchild = nullptr;        // template counters (large children only)
+    int32_t *small_lptr = nullptr;
+    int32_t *bar = nullptr;           // grid barrier: [count, generation]
     int32_t *counters = nullptr;      // scratch counters
     int64_t *l_export = nullptr;
     int64_t *perm = nullptr;          // internal position -> original index
