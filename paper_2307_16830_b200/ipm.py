@@ -253,6 +253,19 @@ class _DeviceSolve:
             self.sl, self.su, ws.dxl, ws.dxu, ws.dsl, ws.dsu, ws.sigma_x, ws.sigma_s, self.grad,
             self.c, ws.a_vals, self.dual_x, self.dual_s, self.primal)))
 
+    def read_async(self, lo, hi):
+        """Start copying scal[lo:hi] and the flag words; returns the event to wait on."""
+        D.TRANSFER["d2h"] += 8 * (hi - lo) + 8
+        self.host[lo:hi].copy_(self.scal[lo:hi], non_blocking=True)
+        self.host_flags.copy_(self.flags, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev
+
+    def read_wait(self, ev, lo, hi):
+        ev.synchronize()
+        return self.host[lo:hi].numpy(), int(self.host_flags[0]), int(self.host_flags[1])
+
     def read(self, lo, hi):
         """Copy scal[lo:hi] and both flag words to the host (one stream sync)."""
         D.TRANSFER["d2h"] += 8 * (hi - lo) + 8
@@ -381,12 +394,21 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal),
                                     stream))
         P.flags[0:1].copy_(ev_flags)
-        sc, adf, ipf = P.read(0, 49)
+        ev_prep = P.read_async(0, 49)
+        # the condensed matrix does not depend on mu: assemble and factor it
+        # (delta_w = delta_c = 0, the first try of kkt.py:424-447) while the
+        # host reads the residuals and runs the barrier update; the PD flag is
+        # checked with the first refinement read
+        t_lin = timer.start()
+        ws.delta_w = ws.delta_c = 0.0
+        backend.factorize_async()
+        sc, adf, ipf = P.read_wait(ev_prep, 0, 49)
         check_ipm_flags(ipf)
         if adf:
             try:
                 ev.raise_on_flags(adf)
             except NonFiniteResult as exc:
+                backend.n_factorizations -= 1
                 return finish(EVAL_ERROR, str(exc))
         fval = float(sc[48])
         S0 = L.PREP_S
@@ -400,6 +422,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         e_0 = resid(0)
         if e_0 < opts.tol:
             report.residual_scaled = e_0
+            backend.n_factorizations -= 1   # the speculative factorisation is not used
             return finish(OPTIMAL)
         k = 1
         e_mu = resid(k)
@@ -426,14 +449,12 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         pv = PVec.empty(n, m)
         pvc = pv.c_struct()
         L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), stream))
-        t0 = timer.start()
+        t0 = t_lin
         try:
-            # speculative: factor with delta_w = delta_c = 0 and solve without
-            # reading the pivot flag; it comes back with the first refinement
-            # read, and only a failure falls back to the regularisation
-            # schedule of solve_with_regularization (kkt.py:424-447)
-            ws.delta_w = ws.delta_c = 0.0
-            backend.factorize_async()
+            # the speculative factorisation above is used without reading the
+            # pivot flag; it comes back with the first refinement read, and
+            # only a failure falls back to the regularisation schedule of
+            # solve_with_regularization (kkt.py:424-447)
             dx, ds, dy = backend.solve_pvec(pv)
             delta_w = 0.0
             steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
