@@ -413,7 +413,10 @@ def main():
             if world > 1:
                 dist.all_reduce(et, op=dist.ReduceOp.MAX)
             return {"value": float(et.item()), "unit": "s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "status": r2.status, "iterations": r2.iterations}
+                    "d2h_bytes_per_step": int(d2h), "status": r2.status, "iterations": r2.iterations,
+                    "steps_s": [round(t, 4) for t in ts],
+                    "last_setup_s": {k: round(v, 4) for k, v in r2.debug.get("setup_seconds", {}).items()},
+                    "last_ipm_s": {k: round(v, 4) for k, v in r2.seconds.items()}}
 
         e2e = timed(SolverOptions(tol=args.tol, ordering=perm))
         e2e["ordering"] = "injected host array (loop-fair, as the CPU baseline)"
@@ -455,6 +458,14 @@ def main():
                                "frac": ach / peak, "alg_bytes_per_launch": nbytes,
                                "mean_launch_ms": ph["mean_ms"]}
 
+    # DRAM traffic of one refactorisation from the committed ncu capture of
+    # the same kernels (profiles/, tools/profile_round.sh), C3 only
+    traffic = None
+    tpath = os.path.join(HERE, "profiles", "r01_traffic_C3.json")
+    if args.workload == "C3" and os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("refactor_bytes_per_launch")
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -479,10 +490,11 @@ def main():
                    "parallelism": "replicas" if world > 1 else "single instance"},
         "iterations": iters, "objective": rep.objective, "status": rep.status,
         "per_iter_ms": per_iter,
-        "roofline": {"bound": "hbm", "kernel": "mf_factor_kernel (refactor)",
+        "roofline": {"bound": "hbm", "kernel": "refactorisation (mf_factor_small + mf_factor_large + mf_factor_top)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": None, "alg_bytes_per_launch": alg_bytes,
+                     "traffic": traffic, "traffic_source": "profiles/r01_traffic_C3.json (ncu, cold L2)",
+                     "alg_bytes_per_launch": alg_bytes,
                      "mean_launch_ms": ref["mean_ms"]},
         "rooflines_secondary": secondary,
         "cpu_baseline": cpu,

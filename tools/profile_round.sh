@@ -4,7 +4,7 @@ set -x
 timeout 1200 python bench.py > gpurun_out/bench_C3.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_C3.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:mf_factor -c 3 -s 30 \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:mf_factor -c 3 -s 9 \
     -o gpurun_out/factor_full python tools/chol_once.py C3 > gpurun_out/ncu_factor_full.log 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"ad_records|ad_gather|assemble_kernel" -c 3 -s 6 \
     -o gpurun_out/ad_full python tools/chol_once.py C3 > gpurun_out/ncu_ad_full.log 2>&1
