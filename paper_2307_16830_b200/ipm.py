@@ -377,6 +377,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     ft_ptr = L.ptr(P.scal[49:50])
     ev_flags = ev.flags
 
+    pv_buf = PVec.empty(n, m)
     for _ in range(opts.max_iter):
         mu = state["mu"]
         # ---- derivatives at x (ipm.py:384-391)
@@ -446,7 +447,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         for lsum in (sc[2], sc[3], sc[S0 + 5], sc[S0 + 6]):
             phi_cur -= mu * float(lsum)
         # ---- Newton step (ipm.py:434-453)
-        pv = PVec.empty(n, m)
+        pv = pv_buf          # overwritten in full by gn_ipm_pvec
         pvc = pv.c_struct()
         L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), stream))
         t0 = t_lin

@@ -52,6 +52,11 @@ class RegState:
 class _Vec7:
     """Seven device vectors (x, s, y, zxl, zxu, zsl, zsu)."""
 
+    def __setattr__(self, name, value):
+        object.__setattr__(self, name, value)
+        if name in FIELDS:
+            object.__setattr__(self, "_cs", None)   # pointer struct is rebuilt on demand
+
     def __init__(self, x, s, y, zxl, zxu, zsl, zsu):
         self.x, self.s, self.y = D.to_dev(x), D.to_dev(s), D.to_dev(y)
         self.zxl, self.zxu = D.to_dev(zxl), D.to_dev(zxu)
@@ -68,7 +73,11 @@ class _Vec7:
         return [getattr(self, f) for f in FIELDS]
 
     def c_struct(self) -> L.Vec7:
-        return L.Vec7(*(t.data_ptr() for t in self.parts()))
+        cs = getattr(self, "_cs", None)
+        if cs is None:
+            cs = L.Vec7(*(t.data_ptr() for t in self.parts()))
+            object.__setattr__(self, "_cs", cs)
+        return cs
 
     def numpy(self):
         return [D.to_host(t) for t in self.parts()]
@@ -210,10 +219,24 @@ class KKTWorkspace:
         L.check(lib.gn_kkt_sigma(self.m, *(L.ptr(t) for t in (self.dsl, self.dsu, self.zsl,
                                                                 self.zsu, self.sigma_s)), st))
 
+    _STATE_FIELDS = ("w_vals", "a_vals", "dxl", "dxu", "dsl", "dsu", "zxl", "zxu", "zsl", "zsu",
+                     "sigma_x", "sigma_s")
+
+    def __setattr__(self, name, value):
+        object.__setattr__(self, name, value)
+        if name in KKTWorkspace._STATE_FIELDS:
+            object.__setattr__(self, "_state", None)
+
     def state(self) -> L.KktState:
-        return L.KktState(*(t.data_ptr() for t in (
-            self.w_vals, self.a_vals, self.dxl, self.dxu, self.dsl, self.dsu, self.zxl, self.zxu,
-            self.zsl, self.zsu, self.sigma_x, self.sigma_s)), float(self.delta_w), float(self.delta_c))
+        """The C struct of device pointers + (delta_w, delta_c); rebuilt only
+        when a buffer is rebound or a regularisation changes."""
+        key = (float(self.delta_w), float(self.delta_c))
+        st = getattr(self, "_state", None)
+        if st is None or getattr(self, "_state_key", None) != key:
+            st = L.KktState(*(getattr(self, f).data_ptr() for f in KKTWorkspace._STATE_FIELDS), *key)
+            object.__setattr__(self, "_state", st)
+            object.__setattr__(self, "_state_key", key)
+        return st
 
     # -- matrix-vector products ----------------------------------------------
     def _mv(self, kind, vals, v, n_out):

@@ -24,11 +24,11 @@ def reset() -> None:
     _spans.clear()
 
 
+_NULL = contextlib.nullcontext()
+
+
 @contextlib.contextmanager
-def span(name: str):
-    if not _enabled:
-        yield
-        return
+def _span(name: str):
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
@@ -37,6 +37,11 @@ def span(name: str):
     finally:
         b.record()
         _spans[name].append((a, b))
+
+
+def span(name: str):
+    """Event pair around a phase when profiling is on; a shared no-op otherwise."""
+    return _span(name) if _enabled else _NULL
 
 
 def summary() -> dict:
