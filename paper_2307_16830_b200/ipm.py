@@ -199,45 +199,55 @@ class _DeviceSolve:
         self.ev = evaluator(model)
         dev = D.require_cuda()
         self.dev = dev
-        # frozen gradient scaling at x0 (ipm.py:179-193)
+        self.obj_scale = 1.0
+        # frozen gradient scaling at x0 (ipm.py:179-193), on the device: the
+        # scale factors, the relaxed slack bounds and the initial slacks are
+        # torch ops; one scalar read later brings obj_scale and theta0 back
         x0d = D.to_dev(self.x0)
         g0 = D.empty(n)
         j0 = D.empty(max(1, model.nnz_jac))
         self.ev.flags.zero_()
         self.ev.launch(x0d, GRAD | JAC, grad=g0, jac=j0)
-        fl = int(self.ev.flags.item())
-        self.ev.raise_on_flags(fl)
-        g0h, j0h = D.to_host(g0), D.to_host(j0)[:model.nnz_jac]
-        if opts.scaling:
-            gm = float(np.abs(g0h).max()) if n else 0.0
-            self.obj_scale = min(1.0, 100.0 / gm) if gm > 0 else 1.0
-            rmax = np.zeros(m)
-            if j0h.size:
-                np.maximum.at(rmax, model.jac_rows, np.abs(j0h))
-            self.con_scale_h = np.ones(m)
-            pos = rmax > 0
-            self.con_scale_h[pos] = np.minimum(1.0, 100.0 / rmax[pos])
-        else:
-            self.obj_scale, self.con_scale_h = 1.0, np.ones(m)
+        self.flags0 = self.ev.flags.clone()
         if ranges is None:
             self.rlo, self.rhi = np.zeros(m), np.zeros(m)
         else:
             r = np.asarray(ranges, dtype=float)
             self.rlo, self.rhi = r[:, 0].copy(), r[:, 1].copy()
-        scaled = np.column_stack([self.rlo * self.con_scale_h, self.rhi * self.con_scale_h]) if m else None
-        self.sl_h, self.su_h = relax_equalities(m, scaled, self.tol_r)
+        if opts.scaling:
+            gm = g0.abs().max() if n else torch.zeros((), dtype=torch.float64, device=dev)
+            self.obj_scale_d = torch.where(gm > 0, torch.clamp(100.0 / gm, max=1.0), torch.ones_like(gm))
+            if m:
+                rmax = torch.zeros(m, dtype=torch.float64, device=dev)
+                if model.nnz_jac:
+                    rmax.scatter_reduce_(0, model.jac_rows_device(), j0[:model.nnz_jac].abs(), "amax")
+                self.con_scale = torch.where(rmax > 0, torch.clamp(100.0 / rmax, max=1.0),
+                                             torch.ones_like(rmax))
+            else:
+                self.con_scale = D.zeros(1)
+        else:
+            self.obj_scale_d = torch.ones((), dtype=torch.float64, device=dev)
+            self.con_scale = torch.ones(max(1, m), dtype=torch.float64, device=dev)
+        # relax_equalities (ipm.py:112-123) on the scaled ranges
+        if m:
+            tol = self.tol_r
+            rlo_d, rhi_d = D.to_dev(self.rlo), D.to_dev(self.rhi)
+            lo, hi = rlo_d * self.con_scale, rhi_d * self.con_scale
+            one = torch.ones_like(lo)
+            inf = torch.full_like(lo, np.inf)
+            self.sl = torch.where(torch.isfinite(lo), lo - tol * torch.maximum(one, lo.abs()), -inf)
+            self.su = torch.where(torch.isfinite(hi), hi + tol * torch.maximum(one, hi.abs()), inf)
+        else:
+            self.sl, self.su = D.zeros(1), D.zeros(1)
+        # scaling keeps finiteness, so the bound count needs no device data
         self.n_bounds = int(np.isfinite(xl).sum() + np.isfinite(xu).sum()
-                            + np.isfinite(self.sl_h).sum() + np.isfinite(self.su_h).sum())
-        # device state
-        td = lambda a: D.to_dev(a)
-        self.xl, self.xu, self.sl, self.su = td(xl), td(xu), td(self.sl_h), td(self.su_h)
-        self.con_scale = td(self.con_scale_h) if m else D.zeros(1)
+                            + np.isfinite(self.rlo).sum() + np.isfinite(self.rhi).sum())
+        self.xl, self.xu = D.to_dev(xl), D.to_dev(xu)
         self.x = x0d.clone()
         self.s, self.y = D.zeros(m), D.zeros(m)
-        self.zxl = td(np.where(np.isfinite(xl), 1.0, 0.0))
-        self.zxu = td(np.where(np.isfinite(xu), 1.0, 0.0))
-        self.zsl = td(np.where(np.isfinite(self.sl_h), 1.0, 0.0))
-        self.zsu = td(np.where(np.isfinite(self.su_h), 1.0, 0.0))
+        fin = lambda t: torch.isfinite(t).to(torch.float64)
+        self.zxl, self.zxu = fin(self.xl), fin(self.xu)
+        self.zsl, self.zsu = (fin(self.sl), fin(self.su)) if m else (D.zeros(0), D.zeros(0))
         self.grad, self.c = D.empty(n), D.empty(max(1, m))
         self.dual_x, self.dual_s, self.primal = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
         self.xt, self.st, self.ct = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
@@ -328,13 +338,20 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         report.final_mu = state["mu"]
         report.x = D.to_host(P.x)
         try:
-            from .autodiff import eval_constraints, eval_objective
-
-            report.objective = eval_objective(model, P.x)
-            g = D.to_host(eval_constraints(model, P.x)) if m else np.zeros(0)
-            report.constraint_violation = (float(np.maximum(np.maximum(P.rlo - g, 0.0),
-                                                            np.maximum(g - P.rhi, 0.0)).max())
-                                           if m else 0.0)
+            # unscaled objective and bound violation of g(x) (ipm.py:350-357)
+            ev.flags.zero_()
+            ev.launch(P.x, F | C, f=P.scal[62:63], c=P.ct)
+            if m:
+                g = P.ct[:m]
+                zero = torch.zeros_like(g)
+                viol = torch.maximum(torch.maximum(D.to_dev(P.rlo) - g, zero),
+                                     torch.maximum(g - D.to_dev(P.rhi), zero))
+                P.scal[63] = viol.max()
+            P.flags[0:1].copy_(ev.flags)
+            fin, adf, _ = P.read(62, 64)
+            ev.raise_on_flags(adf)
+            report.objective = float(fin[0])
+            report.constraint_violation = float(fin[1]) if m else 0.0
         except NonFiniteResult:
             pass
         sec = timer.totals()
@@ -358,19 +375,37 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         if ipm_flags & 4:
             raise DegenerateInterior("s slack lost strict interiority")
 
-    # initial slacks from g(x0) (ipm.py:371-380)
+    # initial slacks from g(x0) (ipm.py:371-380), on the device; one read
+    # returns obj_scale, theta0 and the flags of both evaluations at x0
     P.flags.zero_()
     ev.flags.zero_()
     t0 = timer.start()
     ev.launch(P.x, C, con_scale=P.con_scale, c=P.c)
     timer.stop("ad", t0)
-    torch.cuda.current_stream().synchronize()
-    if int(ev.flags.item()):
+    if m:
+        tol_r, push = P.tol_r, opts.bound_push
+        g0 = P.c[:m]
+        inf = torch.full_like(g0, np.inf)
+        lo = torch.where(torch.isfinite(P.sl), P.sl + push * tol_r, -inf)
+        hi = torch.where(torch.isfinite(P.su), P.su - push * tol_r, inf)
+        s0 = torch.minimum(torch.maximum(g0, lo), hi)
+        s0 = torch.where(lo > hi, 0.5 * (P.sl + P.su), s0)
+        P.s.copy_(s0)
+        P.scal[60] = (g0 - s0).abs().sum()
+    P.scal[61] = P.obj_scale_d
+    P.flags[0:1].copy_(ev.flags)
+    P.flags[1:2].copy_(P.flags0)
+    sc0, adf0, adf_x0 = P.read(60, 62)
+    if adf_x0:
+        try:
+            ev.raise_on_flags(adf_x0, order=(GRAD, JAC))
+        except NonFiniteResult as exc:
+            return finish(EVAL_ERROR, str(exc))
+    P.flags.zero_()
+    if adf0:
         return finish(EVAL_ERROR, "constraint evaluation produced a non-finite value")
-    g0 = D.to_host(P.c)[:m]
-    s0 = initial_slacks(g0, P.sl_h, P.su_h, P.tol_r, opts.bound_push)
-    P.s.copy_(D.to_dev(s0)) if m else None
-    theta0 = float(np.abs(g0 - s0).sum()) if m else 0.0
+    P.obj_scale = float(sc0[1])
+    theta0 = float(sc0[0]) if m else 0.0
     theta_min = 1e-4 * max(1.0, theta0)
     theta_max = 1e4 * max(1.0, theta0)
     f_ptr = L.ptr(P.scal[48:49])
