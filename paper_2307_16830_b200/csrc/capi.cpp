@@ -1,5 +1,8 @@
 // Error reporting and launch/transfer accounting for the C-ABI (gridopf.h).
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "internal.h"
@@ -11,6 +14,21 @@ static std::atomic<int64_t> g_h2d{0};
 void set_error(const std::string &msg) { g_last_error = msg; }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 void count_h2d(size_t bytes) { g_h2d.fetch_add(static_cast<int64_t>(bytes), std::memory_order_relaxed); }
+
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static bool timing_on() {
+  static const bool on = [] {
+    const char *e = std::getenv("GN_HOST_TIMING");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+PhaseTimer::PhaseTimer(const char *n) : name(n), t0(timing_on() ? now_s() : 0.0) {}
+PhaseTimer::~PhaseTimer() {
+  if (timing_on()) std::fprintf(stderr, "[gn host] %-28s %8.2f ms\n", name, 1e3 * (now_s() - t0));
+}
 }  // namespace gn
 
 extern "C" const char *gn_last_error(void) { return gn::g_last_error.c_str(); }

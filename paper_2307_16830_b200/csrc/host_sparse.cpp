@@ -80,6 +80,7 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
     np += (en - st) * (en - st + 1) / 2;
     st = en;
   }
+  PhaseTimer tm_all("condense");
   std::vector<int32_t> rows, cols;
   rows.reserve(nh + n + np);
   cols.reserve(nh + n + np);
@@ -112,7 +113,10 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
     st = en;
   }
   std::vector<int64_t> slot;
-  csc_from_coords(n, rows, cols, C.indptr, C.indices, slot);
+  {
+    PhaseTimer tm("condense.csc_from_coords");
+    csc_from_coords(n, rows, cols, C.indptr, C.indices, slot);
+  }
   C.w_map.assign(slot.begin(), slot.begin() + nh);
   C.diag_map.assign(slot.begin() + nh, slot.begin() + nh + n);
   C.ata_map.assign(slot.begin() + nh + n, slot.end());
@@ -213,6 +217,7 @@ static void min_degree(int64_t n, const int64_t *indptr, const int64_t *indices,
 // ------------------------------------------------------ symbolic Cholesky
 static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_t *indices,
                      const int64_t *perm) {
+  PhaseTimer tm("symbolic");
   S.n = n;
   int64_t nnz = indptr[n];
   S.nnz_a = nnz;
@@ -299,6 +304,7 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
 // relaxed: a column joins the running supernode when the explicit zeros stay
 // below a width-dependent fraction (CHOLMOD-style amalgamation rule).
 static void front_plan(Symbolic &S) {
+  PhaseTimer tm("front_plan");
   const int64_t n = S.n;
   std::vector<int64_t> cc(n);
   for (int64_t j = 0; j < n; ++j) cc[j] = S.l_colptr[j + 1] - S.l_colptr[j];
@@ -375,51 +381,63 @@ static void front_plan(Symbolic &S) {
     for (int64_t J = 0; J < nf; ++J)
       if (S.f_parent[J] >= 0) S.f_child[fl[S.f_parent[J]]++] = static_cast<int32_t>(J);
   }
-  auto local = [&](int64_t J, int64_t row) -> int64_t {
-    const int32_t *b = S.f_rows.data() + S.f_rows_off[J];
-    const int32_t *e = S.f_rows.data() + S.f_rows_off[J + 1];
-    const int32_t *it = std::lower_bound(b, e, static_cast<int32_t>(row));
-    GN_REQUIRE(it != e && *it == row, "row missing from front structure");
-    return it - b;
+  // local row positions through a dense position map filled per front
+  // (O(1) lookups instead of binary searches)
+  std::vector<int32_t> pos(n, -1);
+  auto fill_pos = [&](int64_t J, int32_t v_or_clear) {
+    for (int64_t q = S.f_rows_off[J]; q < S.f_rows_off[J + 1]; ++q)
+      pos[S.f_rows[q]] = v_or_clear < 0 ? -1 : static_cast<int32_t>(q - S.f_rows_off[J]);
   };
-  // relmaps: child update rows (rows past its pivot block) in the parent front
-  S.f_relmap_off.assign(nf + 1, 0);
-  S.relmap.clear();
-  for (int64_t C = 0; C < nf; ++C) {
-    int64_t w = S.f_ncols[C], s = S.f_nrows[C], P = S.f_parent[C];
-    if (P >= 0)
-      for (int64_t i = w; i < s; ++i)
-        S.relmap.push_back(static_cast<int32_t>(local(P, S.f_rows[S.f_rows_off[C] + i])));
-    else
-      GN_REQUIRE(s == w, "root front with an update block");
-    S.f_relmap_off[C + 1] = static_cast<int64_t>(S.relmap.size());
-  }
-  // A scatter (permuted lower entries, grouped by front)
+  // A entries grouped by front
   std::vector<int64_t> per(nf + 1, 0);
   for (int64_t k = 0; k < n; ++k)
     for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) per[snode_of[S.a_rowcol[t]] + 1]++;
   for (int64_t J = 0; J < nf; ++J) per[J + 1] += per[J];
   S.f_a_ptr = per;
-  S.a_kslot.assign(per[nf], 0);
-  S.a_fpos.assign(per[nf], 0);
+  std::vector<int64_t> a_row(per[nf]), a_t(per[nf]);
   {
     std::vector<int64_t> fl(per.begin(), per.end() - 1);
     for (int64_t k = 0; k < n; ++k)
       for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
-        int64_t j = S.a_rowcol[t];
-        int64_t J = snode_of[j];
-        int64_t lr = local(J, k), lc = j - S.f_first[J];
-        int64_t q = fl[J]++;
-        S.a_kslot[q] = S.a_srcslot[t];
-        S.a_fpos[q] = S.f_off[J] + lc * S.f_nrows[J] + lr;
+        const int64_t q = fl[snode_of[S.a_rowcol[t]]]++;
+        a_row[q] = k;
+        a_t[q] = t;
       }
   }
-  // reference L layout -> front storage
+  // relmap offsets (child update rows, in child order)
+  S.f_relmap_off.assign(nf + 1, 0);
+  for (int64_t C = 0; C < nf; ++C) {
+    const int64_t w = S.f_ncols[C], sC = S.f_nrows[C];
+    if (S.f_parent[C] < 0) GN_REQUIRE(sC == w, "root front with an update block");
+    S.f_relmap_off[C + 1] = S.f_relmap_off[C] + (S.f_parent[C] >= 0 ? sC - w : 0);
+  }
+  S.relmap.assign(S.f_relmap_off[nf], 0);
+  S.a_kslot.assign(per[nf], 0);
+  S.a_fpos.assign(per[nf], 0);
   S.l_export.assign(S.l_rowidx.size(), 0);
-  for (int64_t j = 0; j < n; ++j) {
-    int64_t J = snode_of[j], lc = j - S.f_first[J];
-    for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p)
-      S.l_export[p] = S.f_off[J] + lc * S.f_nrows[J] + local(J, S.l_rowidx[p]);
+  for (int64_t J = 0; J < nf; ++J) {
+    fill_pos(J, 0);
+    const int64_t sJ = S.f_nrows[J];
+    auto local = [&](int64_t row) -> int64_t {
+      const int32_t v = pos[row];
+      GN_REQUIRE(v >= 0, "row missing from front structure");
+      return v;
+    };
+    for (int32_t e = S.f_child_ptr[J]; e < S.f_child_ptr[J + 1]; ++e) {   // children's relmaps
+      const int64_t C = S.f_child[e], w = S.f_ncols[C], sC = S.f_nrows[C];
+      int64_t o = S.f_relmap_off[C];
+      for (int64_t i = w; i < sC; ++i) S.relmap[o++] = static_cast<int32_t>(local(S.f_rows[S.f_rows_off[C] + i]));
+    }
+    for (int64_t q = per[J]; q < per[J + 1]; ++q) {   // A scatter
+      const int64_t t = a_t[q], j = S.a_rowcol[t];
+      S.a_kslot[q] = S.a_srcslot[t];
+      S.a_fpos[q] = S.f_off[J] + (j - S.f_first[J]) * sJ + local(a_row[q]);
+    }
+    for (int64_t j = S.f_first[J]; j < S.f_first[J] + S.f_ncols[J]; ++j) {   // reference L layout
+      const int64_t base = S.f_off[J] + (j - S.f_first[J]) * sJ;
+      for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p) S.l_export[p] = base + local(S.l_rowidx[p]);
+    }
+    fill_pos(J, -1);
   }
   // levels (leaves 0) and task order
   S.level.assign(nf, 0);

@@ -33,6 +33,14 @@ inline void sort_unique(std::vector<uint64_t> &k) {
 
 void set_error(const std::string &msg);
 
+// GN_HOST_TIMING=1 prints the duration of instrumented host phases (stderr)
+struct PhaseTimer {
+  const char *name;
+  double t0;
+  explicit PhaseTimer(const char *n);
+  ~PhaseTimer();
+};
+
 struct Error : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
