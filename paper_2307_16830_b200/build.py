@@ -49,6 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(LIB_DIR, "obj", os.path.basename(src) + ".o")
         cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+        if src.endswith(".cpp"):
+            cmd += ["-Xcompiler", "-fopenmp"]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), cmd))
@@ -65,7 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError("libgridopf build failed")
     tmp = LIB + ".tmp"
     # libnvrtc / libcuda are dlopen'ed at run time (ad_codegen.cpp)
-    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-ldl"])
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart", "-ldl", "-lgomp"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -8,6 +8,8 @@
 //   amd_order           amd.py:18-54        (greedy MD, key (deg, deg0, index))
 //   symbolic_cholesky   cholesky.py:94-144  (permute, etree 56-70, row
 //                                            patterns 73-91, L CSC)
+#include <omp.h>
+
 #include <cstring>
 #include <queue>
 #include <tuple>
@@ -22,41 +24,71 @@ namespace gn {
 static void csc_from_coords(int64_t n, const std::vector<int32_t> &rows, const std::vector<int32_t> &cols,
                             std::vector<int64_t> &indptr, std::vector<int64_t> &indices,
                             std::vector<int64_t> &slot) {
-  const size_t K = rows.size();
+  const int64_t K = static_cast<int64_t>(rows.size());
+  for (int64_t t = 0; t < K; ++t) GN_REQUIRE(cols[t] >= 0 && cols[t] < n, "column out of range");
+  // bucket the coordinates by column: per-thread histograms over contiguous
+  // input chunks keep the bucket order stable (deterministic)
+  const int nt = std::max(1, std::min(omp_get_max_threads(), static_cast<int>(K / 65536 + 1)));
+  std::vector<std::vector<int64_t>> hist(nt, std::vector<int64_t>(n + 1, 0));
+  auto chunk = [&](int t) { return std::make_pair(K * t / nt, K * (t + 1) / nt); };
+#pragma omp parallel for num_threads(nt) schedule(static, 1)
+  for (int t = 0; t < nt; ++t) {
+    auto [lo, hi] = chunk(t);
+    for (int64_t q = lo; q < hi; ++q) hist[t][cols[q]]++;
+  }
   std::vector<int64_t> bptr(n + 1, 0);
-  for (size_t t = 0; t < K; ++t) {
-    GN_REQUIRE(cols[t] >= 0 && cols[t] < n, "column out of range");
-    bptr[cols[t] + 1]++;
-  }
-  for (int64_t c = 0; c < n; ++c) bptr[c + 1] += bptr[c];
-  std::vector<int32_t> bucket(K);   // input index, grouped by column (stable)
-  {
-    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
-    for (size_t t = 0; t < K; ++t) bucket[fill[cols[t]]++] = static_cast<int32_t>(t);
-  }
-  std::vector<int64_t> mark(n, -1), pos(n, 0);
-  std::vector<int32_t> uniq;
-  indptr.assign(n + 1, 0);
-  indices.clear();
-  indices.reserve(K);
-  slot.resize(K);
   for (int64_t c = 0; c < n; ++c) {
-    uniq.clear();
-    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
-      const int32_t r = rows[bucket[q]];
-      if (mark[r] != c) {
-        mark[r] = c;
-        uniq.push_back(r);
+    int64_t run = bptr[c];
+    for (int t = 0; t < nt; ++t) {
+      const int64_t h = hist[t][c];
+      hist[t][c] = run;
+      run += h;
+    }
+    bptr[c + 1] = run;
+  }
+  std::vector<int32_t> bucket(K);
+#pragma omp parallel for num_threads(nt) schedule(static, 1)
+  for (int t = 0; t < nt; ++t) {
+    auto [lo, hi] = chunk(t);
+    for (int64_t q = lo; q < hi; ++q) bucket[hist[t][cols[q]]++] = static_cast<int32_t>(q);
+  }
+  // per column: sorted unique rows (count pass, prefix, fill pass)
+  std::vector<int64_t> ucount(n, 0);
+  indptr.assign(n + 1, 0);
+  slot.resize(K);
+  std::vector<int32_t> urows(K);   // unique rows, at the column's bucket offset
+#pragma omp parallel num_threads(nt)
+  {
+    std::vector<int64_t> mark(n, -1);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t c = 0; c < n; ++c) {
+      int64_t u = bptr[c];
+      for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
+        const int32_t r = rows[bucket[q]];
+        if (mark[r] != c) {
+          mark[r] = c;
+          urows[u++] = r;
+        }
       }
+      std::sort(urows.begin() + bptr[c], urows.begin() + u);
+      ucount[c] = u - bptr[c];
     }
-    std::sort(uniq.begin(), uniq.end());
-    const int64_t base = static_cast<int64_t>(indices.size());
-    for (size_t u = 0; u < uniq.size(); ++u) {
-      pos[uniq[u]] = base + static_cast<int64_t>(u);
-      indices.push_back(uniq[u]);
+  }
+  for (int64_t c = 0; c < n; ++c) indptr[c + 1] = indptr[c] + ucount[c];
+  indices.resize(indptr[n]);
+#pragma omp parallel num_threads(nt)
+  {
+    std::vector<int64_t> pos(n, 0);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t c = 0; c < n; ++c) {
+      const int64_t base = indptr[c];
+      for (int64_t u = 0; u < ucount[c]; ++u) {
+        const int32_t r = urows[bptr[c] + u];
+        indices[base + u] = r;
+        pos[r] = base + u;
+      }
+      for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) slot[bucket[q]] = pos[rows[bucket[q]]];
     }
-    indptr[c + 1] = static_cast<int64_t>(indices.size());
-    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) slot[bucket[q]] = pos[rows[bucket[q]]];
   }
 }
 
@@ -97,20 +129,35 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
   C.ata_row.resize(np);
   C.ata_s1.resize(np);
   C.ata_s2.resize(np);
-  int64_t q = 0;
+  // Jacobian row segments and their product offsets (np.tril_indices order)
+  std::vector<int64_t> seg, poff;
   for (int64_t st = 0; st < nj;) {
     int64_t en = st;
     while (en < nj && jr[en] == jr[st]) ++en;
-    // np.tril_indices(k): row-major over the lower triangle
+    seg.push_back(st);
+    st = en;
+  }
+  seg.push_back(nj);
+  poff.assign(seg.size(), 0);
+  for (size_t g = 0; g + 1 < seg.size(); ++g) {
+    const int64_t k = seg[g + 1] - seg[g];
+    poff[g + 1] = poff[g] + k * (k + 1) / 2;
+  }
+  const int64_t base = nh + n;
+  rows.resize(base + np);
+  cols.resize(base + np);
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t g = 0; g < static_cast<int64_t>(seg.size()) - 1; ++g) {
+    const int64_t st = seg[g], en = seg[g + 1];
+    int64_t q = poff[g];
     for (int64_t la = 0; la < en - st; ++la)
       for (int64_t lb = 0; lb <= la; ++lb, ++q) {
-        rows.push_back(static_cast<int32_t>(jc[st + la]));
-        cols.push_back(static_cast<int32_t>(jc[st + lb]));
+        rows[base + q] = static_cast<int32_t>(jc[st + la]);
+        cols[base + q] = static_cast<int32_t>(jc[st + lb]);
         C.ata_row[q] = jr[st];
         C.ata_s1[q] = st + la;
         C.ata_s2[q] = st + lb;
       }
-    st = en;
   }
   std::vector<int64_t> slot;
   {
@@ -266,25 +313,43 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
         S.parent[i] = k;
       }
     }
-  // row patterns (cholesky.py:73-91)
-  std::vector<int64_t> mark(n, -1);
+  // row patterns (cholesky.py:73-91): etree reach of every row, rows in
+  // parallel (count pass, prefix, fill + sort pass)
   S.row_ptr.assign(n + 1, 0);
-  S.row_cols.clear();
-  std::vector<int64_t> pat;
-  for (int64_t k = 0; k < n; ++k) {
-    pat.clear();
-    mark[k] = k;
-    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
-      int64_t i = S.a_rowcol[t];
-      while (i != -1 && mark[i] != k) {
-        mark[i] = k;
-        pat.push_back(i);
-        i = S.parent[i];
+  {
+    std::vector<int64_t> rc(n, 0);
+#pragma omp parallel
+    {
+      std::vector<int64_t> mark(n, -1);
+#pragma omp for schedule(dynamic, 1024)
+      for (int64_t k = 0; k < n; ++k) {
+        int64_t c = 0;
+        mark[k] = k;
+        for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t)
+          for (int64_t i = S.a_rowcol[t]; i != -1 && mark[i] != k; i = S.parent[i]) {
+            mark[i] = k;
+            ++c;
+          }
+        rc[k] = c;
       }
     }
-    std::sort(pat.begin(), pat.end());
-    S.row_cols.insert(S.row_cols.end(), pat.begin(), pat.end());
-    S.row_ptr[k + 1] = static_cast<int64_t>(S.row_cols.size());
+    for (int64_t k = 0; k < n; ++k) S.row_ptr[k + 1] = S.row_ptr[k] + rc[k];
+    S.row_cols.assign(S.row_ptr[n], 0);
+#pragma omp parallel
+    {
+      std::vector<int64_t> mark(n, -1);
+#pragma omp for schedule(dynamic, 1024)
+      for (int64_t k = 0; k < n; ++k) {
+        int64_t o = S.row_ptr[k];
+        mark[k] = k;
+        for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t)
+          for (int64_t i = S.a_rowcol[t]; i != -1 && mark[i] != k; i = S.parent[i]) {
+            mark[i] = k;
+            S.row_cols[o++] = i;
+          }
+        std::sort(S.row_cols.begin() + S.row_ptr[k], S.row_cols.begin() + o);
+      }
+    }
   }
   // L in CSC, diagonal first, rows increasing (cholesky.py:118-131)
   std::vector<int64_t> counts(n, 1);
