@@ -298,27 +298,55 @@ __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contr
   G.out[o] = G.mode == 0 ? acc : acc * sc;
 }
 
-// Objective: per-block fixed-order tree sums, blocks added in order.
-__global__ void ad_objective_kernel(const int32_t *__restrict__ src, const int64_t *__restrict__ bptr,
-                                    int nblk, const double *__restrict__ contrib, double scale,
-                                    double *f, int32_t *flags) {
-  __shared__ double red[256];
-  double total = 0.0;
-  for (int b = 0; b < nblk; ++b) {
-    double part = 0.0;
-    for (int64_t p = bptr[b] + threadIdx.x; p < bptr[b + 1]; p += blockDim.x) part += contrib[src[p]];
-    red[threadIdx.x] = part;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-      __syncthreads();
+// non-finite check of directly written outputs (the gather does it otherwise)
+__global__ void finite_check_kernel(int64_t n, const double *__restrict__ v, int32_t *flags, int32_t bit) {
+  int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool bad = t < n && !isfinite(v[t]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, bit);
+}
+
+// Objective: the flattened contribution list (block order) in contiguous
+// chunks, one CTA each; fixed-order tree sum per CTA, then the last CTA to
+// finish adds the CTA partials in order (deterministic, no FP atomics).
+constexpr int kObjThreads = 256;
+constexpr int kObjMaxCtas = 128;
+__global__ void __launch_bounds__(kObjThreads)
+ad_objective_kernel(const int32_t *__restrict__ src, int64_t total, const double *__restrict__ contrib,
+                    double scale, double *f, int32_t *flags, double *partials, unsigned *counter) {
+  __shared__ double red[kObjThreads];
+  __shared__ bool last;
+  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = per * blockIdx.x, hi = min(total, lo + per);
+  double part = 0.0;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += 4 * kObjThreads) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t q = p + u * kObjThreads;
+      v[u] = q < hi ? contrib[__ldg(src + q)] : 0.0;
     }
-    total += red[0];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) part += v[u];
+  }
+  red[threadIdx.x] = part;
+  __syncthreads();
+  for (int w = kObjThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    if (!isfinite(total)) atomicOr(flags, GN_AD_F);
-    *f = total * scale;
+    partials[blockIdx.x] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double total_sum = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) total_sum += __ldcg(partials + b);
+    if (!isfinite(total_sum)) atomicOr(flags, GN_AD_F);
+    *f = total_sum * scale;
+    *counter = 0u;
   }
 }
 
@@ -326,6 +354,12 @@ __global__ void ad_objective_kernel(const int32_t *__restrict__ src, const int64
 
 static void release_model(Model &M) {
   if (!M.uploaded) return;
+  dev_free(M.d.jslots);
+  M.d.jslots = nullptr;
+  dev_free(M.d.obj_partials);
+  dev_free(M.d.obj_counter);
+  M.d.obj_partials = nullptr;
+  M.d.obj_counter = nullptr;
   void *ps[] = {M.d.blocks, M.d.tape, M.d.consts, M.d.slots, M.d.var_idx, M.d.params, M.d.targets,
                 M.d.c_ptr, M.d.grad_ptr, M.d.jac_ptr, M.d.hess_ptr, M.d.c_src, M.d.grad_src,
                 M.d.jac_src, M.d.hess_src, M.d.obj_src, M.d.jac_rows, M.d.obj_block_ptr};
@@ -408,6 +442,8 @@ static void upload_model(Model &M) {
   M.d.hess_src = dev_upload(narrow<int32_t>(M.hess_src));
   M.d.obj_src = dev_upload(narrow<int32_t>(M.obj_src));
   M.d.obj_block_ptr = dev_upload(M.obj_block_ptr);
+  M.d.obj_partials = dev_alloc<double>(kObjMaxCtas);
+  M.d.obj_counter = dev_upload(std::vector<unsigned>{0u});
   M.d.n_obj_blocks = static_cast<int32_t>(M.obj_block_ptr.size()) - 1;
   M.d.jac_rows = dev_upload(narrow<int32_t>(M.jac_rows));
   // pattern kernels generated from the tapes (NVRTC, cached per source)
@@ -418,12 +454,21 @@ static void upload_model(Model &M) {
     const std::string src = pattern_source(M, pat);
     M.pattern_fn = compile_patterns(src, M.pattern_error);
     if (M.pattern_fn) {
-      struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off; int pattern, pad; };
+      struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off, jslot_off; int pattern, pad; };
       std::vector<GenBlk> gb(db.size());
-      for (size_t b = 0; b < db.size(); ++b)
+      long long joff = 0;
+      for (size_t b = 0; b < db.size(); ++b) {
+        const bool con = M.blocks[b].kind != 0;
         gb[b] = {db[b].cta_begin, db[b].R, db[b].var_off, db[b].par_off, db[b].tgt_off, db[b].contrib_off,
-                 pat[b], 0};
+                 con ? joff : -1, pat[b], 0};
+        if (con) joff += db[b].R * static_cast<long long>(M.blocks[b].first.size());
+      }
       M.d_genblk = dev_upload(gb);
+      // Jacobian slots with exactly one contribution each -> direct writes
+      M.jac_direct = !M.jac_rows.empty();
+      for (size_t o = 0; o + 1 < M.jac_ptr.size() && M.jac_direct; ++o)
+        M.jac_direct = M.jac_ptr[o + 1] - M.jac_ptr[o] == 1;
+      if (M.jac_direct) M.d.jslots = dev_upload(narrow<int32_t>(M.jac_slots));
     }
   } else {
     M.pattern_error = "disabled by GN_AD_INTERPRETER=1";
@@ -442,7 +487,10 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
     const int32_t *vi = M.d.var_idx, *tg = M.d.targets;
     const double *pa = M.d.params;
     unsigned w = what;
-    void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib};
+    const int32_t *jsl = M.d.jslots;
+    int jdirect = (M.jac_direct && (what & GN_AD_JAC)) ? 1 : 0;
+    double *jac_out = jac;
+    void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib, &jsl, &jac_out, &jdirect};
     GN_REQUIRE(launch_patterns(M.pattern_fn, static_cast<unsigned>(M.n_ctas_rec), st, args),
                "pattern kernel launch failed");
     count_launch();
@@ -465,9 +513,13 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
   ga.begin[0] = 0;
   if (what & GN_AD_C) add(M.m, M.d.c_ptr, M.d.c_src, c, con_scale ? 2 : 0, 1.0, con_scale, nullptr, GN_AD_C);
   if (what & GN_AD_GRAD) add(M.n, M.d.grad_ptr, M.d.grad_src, grad, obj_scale != 1.0 ? 1 : 0, obj_scale, nullptr, nullptr, GN_AD_GRAD);
-  if (what & GN_AD_JAC)
+  if ((what & GN_AD_JAC) && !(M.pattern_fn && M.jac_direct))
     add(static_cast<int64_t>(M.jac_rows.size()), M.d.jac_ptr, M.d.jac_src, jac, con_scale ? 3 : 0, 1.0,
         con_scale, M.d.jac_rows, GN_AD_JAC);
+  if ((what & GN_AD_JAC) && M.pattern_fn && M.jac_direct && !M.jac_rows.empty()) {
+    const int64_t nj = static_cast<int64_t>(M.jac_rows.size());
+    GN_LAUNCH(finite_check_kernel, static_cast<unsigned>((nj + 255) / 256), 256, 0, st, nj, jac, flags, GN_AD_JAC);
+  }
   if (what & GN_AD_HESS)
     add(static_cast<int64_t>(M.hess_rows.size()), M.d.hess_ptr, M.d.hess_src, hess, 0, 1.0, nullptr, nullptr, GN_AD_HESS);
   ga.nseg = ns;
@@ -477,10 +529,11 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
     GN_LAUNCH_CHECK();
   }
   if (what & GN_AD_F) {
-    if (M.d.n_obj_blocks > 0) {
-      GN_LAUNCH(ad_objective_kernel, 1, 256, 0, st, M.d.obj_src, M.d.obj_block_ptr, M.d.n_obj_blocks, contrib,
-                                             obj_scale, f, flags);
-      GN_LAUNCH_CHECK();
+    const int64_t total = static_cast<int64_t>(M.obj_src.size());
+    if (total > 0) {
+      const int g = static_cast<int>(std::min<int64_t>(kObjMaxCtas, (total + 4095) / 4096));
+      GN_LAUNCH(ad_objective_kernel, g, kObjThreads, 0, st, M.d.obj_src, total, contrib, obj_scale, f, flags,
+                M.d.obj_partials, M.d.obj_counter);
     } else {
       GN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), st));
     }
@@ -519,8 +572,11 @@ extern "C" int gn_model_traffic(const gn_model *M, uint32_t what, int64_t *bytes
     };
     if (what & GN_AD_C) b += gather(m.c_ptr, m.c_src, m.m);
     if (what & GN_AD_GRAD) b += gather(m.grad_ptr, m.grad_src, m.n);
-    if (what & GN_AD_JAC) b += gather(m.jac_ptr, m.jac_src, static_cast<int64_t>(m.jac_rows.size())) +
-                               4 * static_cast<int64_t>(m.jac_rows.size());
+    if (what & GN_AD_JAC) {
+      const int64_t nj = static_cast<int64_t>(m.jac_rows.size());
+      // direct writes need the slot map only; the gathered path its CSR + rows
+      b += (m.pattern_fn && m.jac_direct) ? 12 * nj : gather(m.jac_ptr, m.jac_src, nj) + 4 * nj;
+    }
     if (what & GN_AD_HESS) b += gather(m.hess_ptr, m.hess_src, static_cast<int64_t>(m.hess_rows.size()));
     if (what & GN_AD_F) b += 4 * static_cast<int64_t>(m.obj_src.size()) + 8;
     *bytes = b;

@@ -103,7 +103,8 @@ std::string gen_pattern(const Model::HBlock &b, int id) {
   o << "__device__ __forceinline__ void pat_" << id
     << "(long long r, long long R, const int *__restrict__ vi, const double *__restrict__ pa, "
        "const int *__restrict__ tg, const double *__restrict__ x, const double *__restrict__ y, "
-       "const double *__restrict__ cs, double obj_w, unsigned what, double *__restrict__ out) {\n";
+       "const double *__restrict__ cs, double obj_w, unsigned what, double *__restrict__ out, "
+       "const int *__restrict__ js, double *__restrict__ jac, int jdirect) {\n";
   // record data: coalesced SoA loads of the variable indices and parameters
   std::set<int> vs, ps;
   for (int i = 0; i < T; ++i) {
@@ -162,11 +163,23 @@ std::string gen_pattern(const Model::HBlock &b, int id) {
     }
   }
   o << "    if (need_first) {\n";
+  if (!obj) {
+    // every Jacobian slot has exactly one contributor (checked at upload):
+    // write the scaled value straight into J, no contribution round trip
+    o << "      if (jdirect) {\n        const double jsc = cs ? cs[__ldg(tg + r)] : 1.0;\n";
+    for (int k = 0; k < nfirst; ++k) {
+      const int s = b.first[k];
+      o << "        jac[__ldg(js + " << k << " * R + r)] = "
+        << (g.has(s) ? "g" + std::to_string(s) : std::string("0.0")) << " * jsc;\n";
+    }
+    o << "      } else {\n";
+  }
   for (int k = 0; k < nfirst; ++k) {
     const int s = b.first[k];
     o << "      out[" << (1 + k) << " * R + r] = " << (g.has(s) ? "g" + std::to_string(s) : std::string("0.0"))
       << ";\n";
   }
+  if (!obj) o << "      }\n";
   o << "    }\n";
   if (npairs > 0) {
     o << "    if (!need_hess) return;\n";
@@ -290,7 +303,7 @@ __device__ __forceinline__ double powc(double v, double c) {
   if (c == -1.0) return 1.0 / v;
   return pow(v, c);
 }
-struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off; int pattern, pad; };
+struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off, jslot_off; int pattern, pad; };
 )";
 
 // ---------------------------------------------------------- NVRTC / driver
@@ -376,7 +389,7 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
     << ") gn_ad_patterns(const GenBlk *__restrict__ blks, int nblk, const int *__restrict__ var_idx, "
        "const double *__restrict__ params, const int *__restrict__ targets, const double *__restrict__ x, "
        "const double *__restrict__ y, const double *__restrict__ cs, double obj_w, unsigned what, "
-       "double *__restrict__ contrib) {\n"
+       "double *__restrict__ contrib, const int *__restrict__ jslots, double *__restrict__ jac, int jdirect) {\n"
        "  int lo = 0, hi = nblk - 1;\n"
        "  while (lo < hi) {\n"
        "    const int mid = (lo + hi + 1) >> 1;\n"
@@ -389,9 +402,10 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
        "  const double *pa = params + B.par_off;\n"
        "  const int *tg = targets + B.tgt_off;\n"
        "  double *out = contrib + B.contrib_off;\n"
+       "  const int *js = B.jslot_off >= 0 ? jslots + B.jslot_off : jslots;\n"
        "  switch (B.pattern) {\n";
   for (size_t id = 0; id < bodies.size(); ++id)
-    o << "    case " << id << ": pat_" << id << "(r, B.R, vi, pa, tg, x, y, cs, obj_w, what, out); break;\n";
+    o << "    case " << id << ": pat_" << id << "(r, B.R, vi, pa, tg, x, y, cs, obj_w, what, out, js, jac, jdirect); break;\n";
   o << "    default: break;\n  }\n}\n";
   return o.str();
 }

@@ -112,6 +112,7 @@ struct Model {
   void *pattern_fn = nullptr;        // NVRTC-compiled pattern kernel (nullptr: interpreter)
   void *d_genblk = nullptr;          // its per-block table (device)
   std::string pattern_error;         // why the interpreter is used, if it is
+  bool jac_direct = false;           // every J slot has exactly one contribution
   struct Dev {
     DevBlock *blocks = nullptr;
     int32_t *tape = nullptr;  // int4-packed (op, a, b, 0)
@@ -126,6 +127,9 @@ struct Model {
     int32_t *jac_rows = nullptr;
     int64_t *obj_block_ptr = nullptr;
     int32_t n_obj_blocks = 0;
+    int32_t *jslots = nullptr;       // Jacobian slot per constraint contribution (direct writes)
+    double *obj_partials = nullptr;  // objective reduction scratch
+    unsigned *obj_counter = nullptr;
   } d;
   ~Model();
 };
