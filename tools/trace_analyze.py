@@ -11,6 +11,14 @@ def analyse(path):
     nfs = int(d["nf_small"])
     small = np.zeros(len(nrows), bool)
     small[order[:nfs]] = True
+    if "panels" in d:
+        fb = d["panels"].astype(np.float64)[32:]
+        ok = fb[:, 0] > 0
+        if ok.any():
+            b0 = fb[ok][0, 0]
+            print("forward blocks of the last front (us): start  diag-solve  gemv")
+            for row in fb[ok]:
+                print("   %8.1f %6.1f %6.1f" % ((row[0] - b0) / 1e3, (row[1] - row[0]) / 1e3, (row[2] - row[1]) / 1e3))
     for ph, name in enumerate(("factor", "forward", "backward")):
         t = tr[ph].astype(np.float64)
         t0 = t[:, 0][t[:, 0] > 0].min()
@@ -41,7 +49,7 @@ def analyse(path):
             tot = 0.0
             print("  critical chain (root first): front w s  [wait->deps, deps->asm, asm->done] us")
             if "panels" in d:
-                pt = d["panels"].astype(np.float64)
+                pt = d["panels"].astype(np.float64)[:32]
                 ok = pt[:, 0] > 0
                 if ok.any():
                     p0 = pt[ok]
