@@ -134,6 +134,7 @@ void gn_symbolic_destroy(gn_symbolic *sym);
 #define GN_AD_GRAD 4u
 #define GN_AD_JAC 8u
 #define GN_AD_HESS 16u
+#define GN_AD_RESET_FLAGS 256u   /* zero *flags before evaluating (stream-ordered) */
 
 /* Uploads the plan and compiles one straight-line device function per
  * distinct pattern tape (NVRTC, sm_100a, cached per process); without NVRTC

@@ -17,6 +17,7 @@ from . import device as D
 from .model import CompiledModel
 
 F, C, GRAD, JAC, HESS = 1, 2, 4, 8, 16
+RESET = 256   # zero the flag word inside the same C call (no separate fill launch)
 _WHAT_NAME = ((F, "objective"), (C, "constraint"), (GRAD, "gradient"), (JAC, "jacobian"),
               (HESS, "hessian"))
 

@@ -481,6 +481,10 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
                     uint32_t what, double *contrib, int32_t *flags, cudaStream_t st) {
   GN_REQUIRE(M.uploaded, "model not uploaded to the device");
   if (what & GN_AD_HESS) GN_REQUIRE(y != nullptr || M.m == 0, "Hessian needs multipliers");
+  if (what & GN_AD_RESET_FLAGS) {
+    GN_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    what &= ~GN_AD_RESET_FLAGS;
+  }
   if (M.n_ctas_rec > 0 && M.pattern_fn) {
     int nblk = static_cast<int>(M.dblocks.size());
     const void *blk = M.d_genblk;

@@ -24,7 +24,7 @@ import torch
 
 from . import _lib as L
 from . import device as D
-from .autodiff import C, F, GRAD, HESS, JAC, NonFiniteResult, evaluator
+from .autodiff import C, F, GRAD, HESS, JAC, RESET, NonFiniteResult, evaluator
 from .kkt import (CondensedBackend, DegenerateInterior, FactorizationFailed, KKTWorkspace, PVec,
                   RegState, RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
                   solve_with_regularization)
@@ -416,10 +416,9 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     for _ in range(opts.max_iter):
         mu = state["mu"]
         # ---- derivatives at x (ipm.py:384-391)
-        ev_flags.zero_()
         t0 = timer.start()
         with span("ad_full"):
-            ev.launch(P.x, F | C | GRAD | JAC | HESS, y=P.y, obj_weight=P.obj_scale,
+            ev.launch(P.x, F | C | GRAD | JAC | HESS | RESET, y=P.y, obj_weight=P.obj_scale,
                       con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
                       grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
         timer.stop("ad", t0)
@@ -526,10 +525,9 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
                     break
                 L.check(lib.gn_ipm_trial_point(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha,
                                                L.ptr(P.xt), L.ptr(P.st), stream))
-            ev_flags.zero_()
             t0 = timer.start()
             with span("ad_trial"):
-                ev.launch(P.xt, F | C, con_scale=P.con_scale, obj_scale=P.obj_scale,
+                ev.launch(P.xt, F | C | RESET, con_scale=P.con_scale, obj_scale=P.obj_scale,
                           f=P.scal[49:50], c=P.ct)
             timer.stop("ad", t0)
             L.check(lib.gn_ipm_trial_merit(ws.handle, ctypes.byref(V), L.ptr(P.ct), L.ptr(P.xt),

@@ -438,6 +438,17 @@ class RefinementStats:
         return self.final_residual / self.scale
 
 
+def _read4(ws, scal):
+    """scal[0:4] -> host through a pinned buffer (one stream sync)."""
+    pin = getattr(ws, "_pin4", None)
+    if pin is None:
+        pin = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+        object.__setattr__(ws, "_pin4", pin)
+    pin.copy_(scal[0:4], non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return pin.numpy()
+
+
 class FactorizationFailed(RuntimeError):
     """Raised by iterative_refinement(check_factor=...) when the speculative
     factorisation behind ``steps`` was not positive definite."""
@@ -455,7 +466,7 @@ def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None)
     res = ws.residual_full(steps, pv, norm_out=scal[0:2])
     if check_factor is not None:
         scal[3:4].copy_(check_factor)
-    host = scal[0:4].cpu().numpy()
+    host = _read4(ws, scal)
     if check_factor is not None and host[3] < ws.n:
         raise FactorizationFailed("condensed matrix not positive definite")
     scale, rnorm = float(host[2]), float(host[0])
@@ -466,7 +477,7 @@ def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None)
         corr = assemble_steps(ws, res, dx, ds, dy, check=False)
         _bind(ws.handle, steps, corr, 1.0)
         res = ws.residual_full(steps, pv, norm_out=scal[0:2])
-        new = float(scal[0].item())
+        new = float(_read4(ws, scal)[0])
         stats.rounds += 1
         if new >= stats.final_residual:
             _bind(ws.handle, steps, corr, -1.0)
