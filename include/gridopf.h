@@ -173,6 +173,10 @@ int gn_chol_factor(gn_symbolic *sym, const double *kvals, double *fronts,
  * Replaces _solve_kernel/solve (cholesky.py:175-217). */
 int gn_chol_solve(gn_symbolic *sym, const double *fronts, const double *b, double *x,
                   double *ws, void *stream);
+/* The calling thread will run k solves concurrently on k streams: its
+ * persistent kernels (which need every CTA co-resident) are sized to 1/k of
+ * the device from now on (thread-local; default 1). */
+int gn_set_concurrency(int k);
 /* Diagnostics: when trace (device int64[3][n_fronts][4]) is non-NULL the
  * factor / forward / backward kernels stamp %globaltimer per front (task
  * start, dependencies met, assembled, done).  NULL turns it off. */

@@ -80,6 +80,59 @@ def solve_batch(instances, options: SolverOptions | None = None) -> list[SolveRe
     return reports
 
 
+def solve_batch_concurrent(instances, options: SolverOptions | None = None,
+                           workers: int = 4) -> list[SolveReport]:
+    """Solve the instances with `workers` host threads, each driving its own
+    CUDA stream and its own symbolic plan; a 1,358-bus solve is
+    latency-bound and leaves most of the GPU idle, so independent solves
+    overlap.  Every persistent kernel is sized to 1/workers of the device
+    (gn_set_concurrency) so concurrent kernels stay co-resident.  Results
+    are bitwise those of solve_batch (the kernels are deterministic)."""
+    import threading
+
+    import torch
+
+    from . import _lib as L
+
+    opts = options if options is not None else SolverOptions()
+    n = len(instances)
+    workers = max(1, min(int(workers), n))
+    if workers == 1:
+        return solve_batch(instances, opts)
+    dev = torch.cuda.current_device()
+    results: list = [None] * n
+    errors: list = []
+    groups = [list(range(w, n, workers)) for w in range(workers)]
+
+    def run(idxs):
+        try:
+            torch.cuda.set_device(dev)
+            L.check(L.lib().gn_set_concurrency(workers))
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                first = None
+                for i in idxs:
+                    am = instances[i]
+                    if first is not None:
+                        share_symbolic([first, am.model])
+                    results[i] = solve(am.model, opts, constraint_ranges=am.ranges)
+                    first = first or am.model
+            stream.synchronize()
+        except BaseException as exc:   # surfaced in the caller
+            errors.append(exc)
+        finally:
+            L.lib().gn_set_concurrency(1)
+
+    threads = [threading.Thread(target=run, args=(g,)) for g in groups]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    return results
+
+
 def pack_records(reports, n_var: int) -> np.ndarray:
     """[len(reports), n_var + N_META] float64 records."""
     out = np.full((len(reports), n_var + N_META), np.nan)

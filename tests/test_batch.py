@@ -77,3 +77,15 @@ def test_batched_solve_equals_single_solves():
         assert r.status == alone.status == "optimal"
         assert r.iterations == alone.iterations
         np.testing.assert_array_equal(r.x, alone.x)   # deterministic, shared plan
+
+
+@pytest.mark.gpu
+def test_concurrent_batch_is_bitwise_sequential():
+    from paper_2307_16830_b200 import SolverOptions
+
+    opts = SolverOptions(tol=1e-6)
+    seq = B.solve_batch(B.perturbed_instances(4, range(6)), opts)
+    con = B.solve_batch_concurrent(B.perturbed_instances(4, range(6)), opts, workers=3)
+    for a, b in zip(seq, con):
+        assert a.status == b.status == "optimal" and a.iterations == b.iterations
+        np.testing.assert_array_equal(a.x, b.x)
