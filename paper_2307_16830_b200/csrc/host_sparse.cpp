@@ -11,6 +11,7 @@
 #include <omp.h>
 
 #include <cstring>
+#include <new>
 #include <queue>
 #include <tuple>
 
@@ -23,7 +24,8 @@ namespace gn {
 // csc.py:52-76).  Bucketed by column: O(nnz + sum_c u_c log u_c).
 static void csc_from_coords(int64_t n, const std::vector<int32_t> &rows, const std::vector<int32_t> &cols,
                             std::vector<int64_t> &indptr, std::vector<int64_t> &indices,
-                            std::vector<int64_t> &slot) {
+                            std::vector<int64_t> &slot, std::vector<int32_t> *bucket_out = nullptr,
+                            std::vector<int64_t> *bptr_out = nullptr) {
   const int64_t K = static_cast<int64_t>(rows.size());
   for (int64_t t = 0; t < K; ++t) GN_REQUIRE(cols[t] >= 0 && cols[t] < n, "column out of range");
   // bucket the coordinates by column: per-thread histograms over contiguous
@@ -89,6 +91,39 @@ static void csc_from_coords(int64_t n, const std::vector<int32_t> &rows, const s
       }
       for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) slot[bucket[q]] = pos[rows[bucket[q]]];
     }
+  }
+  if (bucket_out) *bucket_out = std::move(bucket);
+  if (bptr_out) *bptr_out = std::move(bptr);
+}
+
+// Stable parallel bucketing: items 0..N-1 with key(i) in [0, nkeys) ->
+// ptr (nkeys+1) and dest(i), the item's slot, ascending i inside a key.
+// Per-thread histograms over contiguous item chunks keep the order stable.
+template <class KeyFn, class PlaceFn>
+static void par_bucket(int64_t nkeys, int64_t N, KeyFn key, PlaceFn place, std::vector<int64_t> &ptr) {
+  const int nt = std::max(1, std::min(omp_get_max_threads(), static_cast<int>(N / 65536 + 1)));
+  std::vector<std::vector<int64_t>> hist(nt);
+  auto chunk = [&](int t) { return std::make_pair(N * t / nt, N * (t + 1) / nt); };
+#pragma omp parallel for num_threads(nt) schedule(static, 1)
+  for (int t = 0; t < nt; ++t) {
+    hist[t].assign(nkeys, 0);
+    auto [lo, hi] = chunk(t);
+    for (int64_t i = lo; i < hi; ++i) hist[t][key(i)]++;
+  }
+  ptr.assign(nkeys + 1, 0);
+  for (int64_t c = 0; c < nkeys; ++c) {
+    int64_t run = ptr[c];
+    for (int t = 0; t < nt; ++t) {
+      const int64_t h = hist[t][c];
+      hist[t][c] = run;
+      run += h;
+    }
+    ptr[c + 1] = run;
+  }
+#pragma omp parallel for num_threads(nt) schedule(static, 1)
+  for (int t = 0; t < nt; ++t) {
+    auto [lo, hi] = chunk(t);
+    for (int64_t i = lo; i < hi; ++i) place(i, hist[t][key(i)]++);
   }
 }
 
@@ -159,14 +194,49 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
         C.ata_s2[q] = st + lb;
       }
   }
-  std::vector<int64_t> slot;
+  std::vector<int64_t> slot, bptr;
+  std::vector<int32_t> bucket;
   {
     PhaseTimer tm("condense.csc_from_coords");
-    csc_from_coords(n, rows, cols, C.indptr, C.indices, slot);
+    csc_from_coords(n, rows, cols, C.indptr, C.indices, slot, &bucket, &bptr);
   }
   C.w_map.assign(slot.begin(), slot.begin() + nh);
   C.diag_map.assign(slot.begin() + nh, slot.begin() + nh + n);
   C.ata_map.assign(slot.begin() + nh + n, slot.end());
+  // assembly plan: the A^T A products grouped by K slot, ascending product
+  // index inside a slot (the summation order of kkt.py:243-283).  The column
+  // buckets already hold every coordinate of a column in input order, and a
+  // slot belongs to one column, so columns are processed independently.
+  PhaseTimer tm_plan("condense.assembly_plan");
+  const int64_t nk = C.indptr[n];
+  GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
+  C.k_ptr.assign(nk + 1, 0);
+  C.k_row.resize(np);
+  C.k_s1.resize(np);
+  C.k_s2.resize(np);
+#pragma omp parallel for schedule(dynamic, 512)
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q)
+      if (bucket[q] >= base) C.k_ptr[slot[bucket[q]] + 1]++;
+  for (int64_t s = 0; s < nk; ++s) C.k_ptr[s + 1] += C.k_ptr[s];
+#pragma omp parallel
+  {
+    std::vector<int32_t> fill;
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t c = 0; c < n; ++c) {
+      const int64_t s0 = C.indptr[c];
+      fill.assign(C.k_ptr.begin() + s0, C.k_ptr.begin() + C.indptr[c + 1]);
+      for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
+        const int64_t t = bucket[q];
+        if (t < base) continue;
+        const int64_t p = t - base;
+        const int32_t d = fill[slot[t] - s0]++;
+        C.k_row[d] = static_cast<int32_t>(C.ata_row[p]);
+        C.k_s1[d] = static_cast<int32_t>(C.ata_s1[p]);
+        C.k_s2[d] = static_cast<int32_t>(C.ata_s2[p]);
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------ ordering
@@ -274,29 +344,30 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
     GN_REQUIRE(perm[k] >= 0 && perm[k] < n && pinv[perm[k]] == -1, "ordering is not a permutation");
     pinv[perm[k]] = k;
   }
+  PhaseTimer tm_perm("symbolic.permute+sort");
   std::vector<int64_t> prow(nnz), pcol(nnz);
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t j = 0; j < n; ++j)
     for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
       int64_t a = pinv[indices[p]], b = pinv[j];
       prow[p] = std::max(a, b);
       pcol[p] = std::min(a, b);
     }
-  // stable sort by (prow, pcol): counting sort on pcol, then on prow
-  std::vector<int64_t> cnt(n + 1), o1(nnz), o2(nnz);
-  for (int64_t p = 0; p < nnz; ++p) cnt[pcol[p] + 1]++;
-  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-  for (int64_t p = 0; p < nnz; ++p) o1[cnt[pcol[p]]++] = p;
-  std::fill(cnt.begin(), cnt.end(), 0);
-  for (int64_t p = 0; p < nnz; ++p) cnt[prow[p] + 1]++;
-  for (int64_t i = 0; i < n; ++i) cnt[i + 1] += cnt[i];
-  S.a_rowptr.assign(cnt.begin(), cnt.end());
-  for (int64_t t = 0; t < nnz; ++t) {
-    int64_t p = o1[t];
-    o2[cnt[prow[p]]++] = p;
-  }
+  // order by (prow, pcol): bucket by prow, then sort each row by pcol (the
+  // pairs are unique, so this is the reference's stable lexicographic order)
+  std::vector<int64_t> o2(nnz);
+  par_bucket(n, nnz, [&](int64_t p) { return prow[p]; }, [&](int64_t p, int64_t d) { o2[d] = p; },
+             S.a_rowptr);
   S.a_rowcol.resize(nnz);
-  S.a_srcslot = o2;
-  for (int64_t t = 0; t < nnz; ++t) S.a_rowcol[t] = pcol[o2[t]];
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t r = 0; r < n; ++r) {
+    std::sort(o2.begin() + S.a_rowptr[r], o2.begin() + S.a_rowptr[r + 1],
+              [&](int64_t x, int64_t y) { return pcol[x] < pcol[y]; });
+    for (int64_t t = S.a_rowptr[r]; t < S.a_rowptr[r + 1]; ++t) S.a_rowcol[t] = pcol[o2[t]];
+  }
+  S.a_srcslot = std::move(o2);
+  tm_perm.~PhaseTimer();
+  new (&tm_perm) PhaseTimer("symbolic.etree");
   // elimination tree (cholesky.py:56-70)
   S.parent.assign(n, -1);
   std::vector<int64_t> anc(n, -1);
@@ -313,6 +384,8 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
         S.parent[i] = k;
       }
     }
+  tm_perm.~PhaseTimer();
+  new (&tm_perm) PhaseTimer("symbolic.row_patterns");
   // row patterns (cholesky.py:73-91): etree reach of every row, rows in
   // parallel (count pass, prefix, fill + sort pass)
   S.row_ptr.assign(n + 1, 0);
@@ -351,16 +424,22 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
       }
     }
   }
-  // L in CSC, diagonal first, rows increasing (cholesky.py:118-131)
-  std::vector<int64_t> counts(n, 1);
-  for (int64_t j : S.row_cols) counts[j]++;
-  S.l_colptr.assign(n + 1, 0);
-  for (int64_t j = 0; j < n; ++j) S.l_colptr[j + 1] = S.l_colptr[j] + counts[j];
-  S.l_rowidx.assign(S.l_colptr[n], 0);
-  std::vector<int64_t> fill(S.l_colptr.begin(), S.l_colptr.end() - 1);
-  for (int64_t j = 0; j < n; ++j) S.l_rowidx[fill[j]++] = j;
+  tm_perm.~PhaseTimer();
+  new (&tm_perm) PhaseTimer("symbolic.L_transpose");
+  // L in CSC, diagonal first, rows increasing (cholesky.py:118-131): a
+  // stable bucketing of the row-pattern entries by column
+  const int64_t nrc = S.row_ptr[n];
+  std::vector<int32_t> rowof(nrc);
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t k = 0; k < n; ++k)
-    for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) S.l_rowidx[fill[S.row_cols[t]]++] = k;
+    for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) rowof[t] = static_cast<int32_t>(k);
+  std::vector<int64_t> cptr;
+  S.l_rowidx.assign(nrc + n, 0);
+  par_bucket(n, nrc, [&](int64_t t) { return S.row_cols[t]; },
+             [&](int64_t t, int64_t d) { S.l_rowidx[d + S.row_cols[t] + 1] = rowof[t]; }, cptr);
+  S.l_colptr.resize(n + 1);
+  for (int64_t j = 0; j <= n; ++j) S.l_colptr[j] = cptr[j] + j;
+  for (int64_t j = 0; j < n; ++j) S.l_rowidx[S.l_colptr[j]] = j;
 }
 
 // ------------------------------------------------------------ front plan
@@ -446,29 +525,17 @@ static void front_plan(Symbolic &S) {
     for (int64_t J = 0; J < nf; ++J)
       if (S.f_parent[J] >= 0) S.f_child[fl[S.f_parent[J]]++] = static_cast<int32_t>(J);
   }
-  // local row positions through a dense position map filled per front
-  // (O(1) lookups instead of binary searches)
-  std::vector<int32_t> pos(n, -1);
-  auto fill_pos = [&](int64_t J, int32_t v_or_clear) {
-    for (int64_t q = S.f_rows_off[J]; q < S.f_rows_off[J + 1]; ++q)
-      pos[S.f_rows[q]] = v_or_clear < 0 ? -1 : static_cast<int32_t>(q - S.f_rows_off[J]);
-  };
-  // A entries grouped by front
-  std::vector<int64_t> per(nf + 1, 0);
+  PhaseTimer tm_maps("front_plan.maps");
+  // A entries grouped by front (ascending row inside a front)
+  const int64_t na = S.a_rowptr[n];
+  std::vector<int32_t> arow(na);
+#pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t k = 0; k < n; ++k)
-    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) per[snode_of[S.a_rowcol[t]] + 1]++;
-  for (int64_t J = 0; J < nf; ++J) per[J + 1] += per[J];
-  S.f_a_ptr = per;
-  std::vector<int64_t> a_row(per[nf]), a_t(per[nf]);
-  {
-    std::vector<int64_t> fl(per.begin(), per.end() - 1);
-    for (int64_t k = 0; k < n; ++k)
-      for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) {
-        const int64_t q = fl[snode_of[S.a_rowcol[t]]]++;
-        a_row[q] = k;
-        a_t[q] = t;
-      }
-  }
+    for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) arow[t] = static_cast<int32_t>(k);
+  std::vector<int64_t> a_t(na);
+  par_bucket(nf, na, [&](int64_t t) { return snode_of[S.a_rowcol[t]]; },
+             [&](int64_t t, int64_t d) { a_t[d] = t; }, S.f_a_ptr);
+  const std::vector<int64_t> &per = S.f_a_ptr;
   // relmap offsets (child update rows, in child order)
   S.f_relmap_off.assign(nf + 1, 0);
   for (int64_t C = 0; C < nf; ++C) {
@@ -477,33 +544,46 @@ static void front_plan(Symbolic &S) {
     S.f_relmap_off[C + 1] = S.f_relmap_off[C] + (S.f_parent[C] >= 0 ? sC - w : 0);
   }
   S.relmap.assign(S.f_relmap_off[nf], 0);
-  S.a_kslot.assign(per[nf], 0);
-  S.a_fpos.assign(per[nf], 0);
+  S.a_kslot.assign(na, 0);
+  S.a_fpos.assign(na, 0);
   S.l_export.assign(S.l_rowidx.size(), 0);
-  for (int64_t J = 0; J < nf; ++J) {
-    fill_pos(J, 0);
-    const int64_t sJ = S.f_nrows[J];
-    auto local = [&](int64_t row) -> int64_t {
-      const int32_t v = pos[row];
-      GN_REQUIRE(v >= 0, "row missing from front structure");
-      return v;
-    };
-    for (int32_t e = S.f_child_ptr[J]; e < S.f_child_ptr[J + 1]; ++e) {   // children's relmaps
-      const int64_t C = S.f_child[e], w = S.f_ncols[C], sC = S.f_nrows[C];
-      int64_t o = S.f_relmap_off[C];
-      for (int64_t i = w; i < sC; ++i) S.relmap[o++] = static_cast<int32_t>(local(S.f_rows[S.f_rows_off[C] + i]));
+  // local row positions through a dense per-thread position map filled per
+  // front (O(1) lookups); every front writes disjoint ranges (its own A
+  // entries, its columns of L, its children's relmaps)
+  int missing = 0;
+#pragma omp parallel reduction(| : missing)
+  {
+    std::vector<int32_t> pos(n, -1);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t J = 0; J < nf; ++J) {
+      const int64_t r0 = S.f_rows_off[J], r1 = S.f_rows_off[J + 1];
+      for (int64_t q = r0; q < r1; ++q) pos[S.f_rows[q]] = static_cast<int32_t>(q - r0);
+      const int64_t sJ = S.f_nrows[J];
+      auto local = [&](int64_t row) -> int64_t {
+        const int32_t v = pos[row];
+        missing |= v < 0;
+        return v < 0 ? 0 : v;
+      };
+      for (int32_t e = S.f_child_ptr[J]; e < S.f_child_ptr[J + 1]; ++e) {   // children's relmaps
+        const int64_t C = S.f_child[e], w = S.f_ncols[C], sC = S.f_nrows[C];
+        int64_t o = S.f_relmap_off[C];
+        for (int64_t i = w; i < sC; ++i)
+          S.relmap[o++] = static_cast<int32_t>(local(S.f_rows[S.f_rows_off[C] + i]));
+      }
+      for (int64_t q = per[J]; q < per[J + 1]; ++q) {   // A scatter
+        const int64_t t = a_t[q], j = S.a_rowcol[t];
+        S.a_kslot[q] = S.a_srcslot[t];
+        S.a_fpos[q] = S.f_off[J] + (j - S.f_first[J]) * sJ + local(arow[t]);
+      }
+      for (int64_t j = S.f_first[J]; j < S.f_first[J] + S.f_ncols[J]; ++j) {   // reference L layout
+        const int64_t base = S.f_off[J] + (j - S.f_first[J]) * sJ;
+        for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p)
+          S.l_export[p] = base + local(S.l_rowidx[p]);
+      }
+      for (int64_t q = r0; q < r1; ++q) pos[S.f_rows[q]] = -1;
     }
-    for (int64_t q = per[J]; q < per[J + 1]; ++q) {   // A scatter
-      const int64_t t = a_t[q], j = S.a_rowcol[t];
-      S.a_kslot[q] = S.a_srcslot[t];
-      S.a_fpos[q] = S.f_off[J] + (j - S.f_first[J]) * sJ + local(a_row[q]);
-    }
-    for (int64_t j = S.f_first[J]; j < S.f_first[J] + S.f_ncols[J]; ++j) {   // reference L layout
-      const int64_t base = S.f_off[J] + (j - S.f_first[J]) * sJ;
-      for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p) S.l_export[p] = base + local(S.l_rowidx[p]);
-    }
-    fill_pos(J, -1);
   }
+  GN_REQUIRE(!missing, "row missing from front structure");
   // levels (leaves 0) and task order
   S.level.assign(nf, 0);
   int64_t maxl = 0;

@@ -139,6 +139,7 @@ struct Condense {
   int64_t n = 0, nnz_h = 0, nnz_j = 0;
   std::vector<int64_t> indptr, indices;
   std::vector<int64_t> w_map, diag_map, ata_map, ata_row, ata_s1, ata_s2;
+  std::vector<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
 };
 
 // ------------------------------------------------------- symbolic factor

@@ -396,22 +396,10 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
       kw[cs->w_map[p]] = static_cast<int32_t>(p);
     }
     for (int64_t i = 0; i < n; ++i) kd[cs->diag_map[i]] = static_cast<int32_t>(i);
-    GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
-    std::vector<int32_t> kp(nk + 1, 0);
-    for (int64_t p = 0; p < np; ++p) kp[cs->ata_map[p] + 1]++;
-    for (int64_t s = 0; s < nk; ++s) kp[s + 1] += kp[s];
-    std::vector<int32_t> krow(np), k1(np), k2(np);
-    std::vector<int32_t> fl(kp.begin(), kp.end() - 1);
-    for (int64_t p = 0; p < np; ++p) {
-      int64_t q = fl[cs->ata_map[p]]++;
-      krow[q] = static_cast<int32_t>(cs->ata_row[p]);
-      k1[q] = static_cast<int32_t>(cs->ata_s1[p]);
-      k2[q] = static_cast<int32_t>(cs->ata_s2[p]);
-    }
-    K.d.k_ptr = dev_upload(kp);
-    K.d.k_row = dev_upload(krow);
-    K.d.k_s1 = dev_upload(k1);
-    K.d.k_s2 = dev_upload(k2);
+    K.d.k_ptr = dev_upload(cs->k_ptr);
+    K.d.k_row = dev_upload(cs->k_row);
+    K.d.k_s1 = dev_upload(cs->k_s1);
+    K.d.k_s2 = dev_upload(cs->k_s2);
     K.d.k_w = dev_upload(kw);
     K.d.k_diag = dev_upload(kd);
     K.has_assembly = true;

@@ -27,7 +27,7 @@ from . import device as D
 from .autodiff import C, F, GRAD, HESS, JAC, RESET, NonFiniteResult, evaluator
 from .kkt import (CondensedBackend, DegenerateInterior, FactorizationFailed, KKTWorkspace, PVec,
                   RegState, RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
-                  solve_with_regularization)
+                  solve_with_regularization, symbolic_condense)
 from .profiling import span
 
 OPTIMAL = "optimal"
@@ -312,9 +312,13 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     cache = getattr(model, "_kkt_cache", None)
     if cache is None or cache[0] != key:
         t0 = time.perf_counter()
-        ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols)
+        cs = symbolic_condense(model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols, n)
+        setup["condense"] = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols,
+                          condensed=cs)
         setup["kkt_workspace"] = time.perf_counter() - t0
-        backend = CondensedBackend(ws, ordering=opts.ordering, timings=setup)
+        backend = CondensedBackend(ws, ordering=opts.ordering, timings=setup, structure=cs)
         model._kkt_cache = (key, ws, backend)
     else:
         _, ws, backend = cache

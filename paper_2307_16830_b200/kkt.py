@@ -335,15 +335,18 @@ def residual_norm(pv) -> float:
 class CondensedBackend:
     """Sparse Cholesky of the condensed primal system on the GPU (kkt.py:286-325)."""
 
-    def __init__(self, ws: KKTWorkspace, ordering=None, timings=None):
+    def __init__(self, ws: KKTWorkspace, ordering=None, timings=None, structure=None):
         import time
 
         tm = timings if timings is not None else {}
-        t = time.perf_counter()
         self.ws = ws
-        self.structure = symbolic_condense(ws.hess_rows, ws.hess_cols, ws.jac_rows, ws.jac_cols, ws.n)
+        if structure is None:
+            t = time.perf_counter()
+            structure = symbolic_condense(ws.hess_rows, ws.hess_cols, ws.jac_rows, ws.jac_cols,
+                                          ws.n)
+            tm["condense"] = time.perf_counter() - t
+        self.structure = structure
         ws.attach_condensed(self.structure)
-        tm["condense"] = time.perf_counter() - t
         t = time.perf_counter()
         if ordering is None:
             ordering = S.amd_order(self.structure.matrix)
