@@ -374,6 +374,7 @@ static void release_model(Model &M) {
 Model::~Model() { release_model(*this); }
 
 static void upload_model(Model &M) {
+  PhaseTimer tm("upload_model");
   std::vector<DevBlock> db;
   std::vector<int4> tape;
   std::vector<double> consts;

@@ -18,12 +18,25 @@ void count_h2d(size_t bytes) { g_h2d.fetch_add(static_cast<int64_t>(bytes), std:
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
-static bool timing_on() {
+static std::atomic<int64_t> g_malloc_ns{0}, g_copy_ns{0}, g_nalloc{0};
+static void print_upload_totals() {
+  std::fprintf(stderr, "[gn host] device allocations %lld: malloc %.2f ms, H2D copies %.2f ms\n",
+               static_cast<long long>(g_nalloc.load()), 1e-6 * g_malloc_ns.load(), 1e-6 * g_copy_ns.load());
+}
+bool timing_on() {
   static const bool on = [] {
     const char *e = std::getenv("GN_HOST_TIMING");
-    return e && e[0] == '1';
+    const bool v = e && e[0] == '1';
+    if (v) std::atexit(print_upload_totals);
+    return v;
   }();
   return on;
+}
+double host_now() { return now_s(); }
+void add_upload_time(double malloc_s, double copy_s) {
+  if (malloc_s > 0) g_nalloc.fetch_add(1);
+  g_malloc_ns.fetch_add(static_cast<int64_t>(malloc_s * 1e9));
+  g_copy_ns.fetch_add(static_cast<int64_t>(copy_s * 1e9));
 }
 PhaseTimer::PhaseTimer(const char *n) : name(n), t0(timing_on() ? now_s() : 0.0) {}
 PhaseTimer::~PhaseTimer() {

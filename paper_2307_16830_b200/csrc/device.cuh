@@ -29,22 +29,27 @@ namespace gn {
 
 void count_launch();
 void count_h2d(size_t bytes);
+bool timing_on();
+double host_now();
+void add_upload_time(double malloc_s, double copy_s);
+
+void *dev_malloc(size_t bytes);   // cached device allocation (alloc.cu)
+void dev_free(void *p);
 
 template <class T>
 T *dev_upload(const std::vector<T> &v) {
-  T *p = nullptr;
-  size_t bytes = sizeof(T) * (v.empty() ? 1 : v.size());
-  GN_CUDA(cudaMalloc(&p, bytes));
+  T *p = static_cast<T *>(dev_malloc(sizeof(T) * (v.empty() ? 1 : v.size())));
+  const bool tm = timing_on();
+  const double t0 = tm ? host_now() : 0.0;
   if (!v.empty()) GN_CUDA(cudaMemcpy(p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  if (tm) add_upload_time(0.0, host_now() - t0);
   count_h2d(sizeof(T) * v.size());
   return p;
 }
 
 template <class T>
 T *dev_alloc(size_t count) {
-  T *p = nullptr;
-  GN_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
-  return p;
+  return static_cast<T *>(dev_malloc(sizeof(T) * (count ? count : 1)));
 }
 
 template <class D, class S>
@@ -54,9 +59,6 @@ std::vector<D> narrow(const std::vector<S> &v) {
   return out;
 }
 
-inline void dev_free(void *p) {
-  if (p) cudaFree(p);
-}
 
 inline int sm_count() {
   int dev = 0, n = 0;

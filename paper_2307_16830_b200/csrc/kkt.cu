@@ -323,6 +323,7 @@ RedSpec max_spec(Kkt &K, double *out) {
 
 static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *hr, const int64_t *hc,
                        int64_t nj, const int64_t *jr, const int64_t *jc, const Condense *cs) {
+  PhaseTimer tm("kkt_create");
   K.n = n;
   K.m = m;
   K.nh = nh;

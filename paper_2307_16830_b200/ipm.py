@@ -25,9 +25,9 @@ import torch
 from . import _lib as L
 from . import device as D
 from .autodiff import C, F, GRAD, HESS, JAC, RESET, NonFiniteResult, evaluator
-from .kkt import (CondensedBackend, DegenerateInterior, FactorizationFailed, KKTWorkspace, PVec,
-                  RegState, RegularizationExhausted, Steps, assemble_steps, iterative_refinement,
-                  solve_with_regularization, symbolic_condense)
+from .kkt import (CondensedBackend, DegenerateInterior, FactorizationFailed, HostAnalysis,
+                  KKTWorkspace, PVec, RegState, RegularizationExhausted, Steps, assemble_steps,
+                  iterative_refinement, solve_with_regularization)
 from .profiling import span
 
 OPTIMAL = "optimal"
@@ -291,6 +291,12 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     t_start = time.perf_counter()
     report = SolveReport(status=MAX_ITER, n_var=model.n_var, n_con=model.n_con)
     setup = {}
+    # symbolic analysis (condensed pattern, ordering, symbolic factor, device
+    # plans) is a function of the sparsity only: cached on the model.  On a
+    # miss its host part starts on a worker thread right away.
+    key = None if opts.ordering is None else id(opts.ordering)
+    cache = getattr(model, "_kkt_cache", None)
+    analysis = HostAnalysis(model, opts.ordering) if cache is None or cache[0] != key else None
     try:
         P = _DeviceSolve(model, opts, constraint_ranges)
         setup["problem"] = time.perf_counter() - t_start
@@ -306,19 +312,19 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     stream = D.stream_ptr()
     timer = _Timer()
 
-    # symbolic analysis (condensed pattern, ordering, symbolic factor, device
-    # plans) is a function of the sparsity only: cached on the model
-    key = None if opts.ordering is None else id(opts.ordering)
-    cache = getattr(model, "_kkt_cache", None)
-    if cache is None or cache[0] != key:
+    if analysis is not None:
         t0 = time.perf_counter()
-        cs = symbolic_condense(model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols, n)
-        setup["condense"] = time.perf_counter() - t0
+        cs = analysis.condensed()
+        setup["wait_condense"] = time.perf_counter() - t0
         t0 = time.perf_counter()
         ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols,
                           condensed=cs)
         setup["kkt_workspace"] = time.perf_counter() - t0
-        backend = CondensedBackend(ws, ordering=opts.ordering, timings=setup, structure=cs)
+        t0 = time.perf_counter()
+        sym = analysis.symbolic()
+        setup["wait_symbolic"] = time.perf_counter() - t0
+        backend = CondensedBackend(ws, timings=setup, structure=cs, symbolic=sym)
+        setup.update({"worker_" + k: v for k, v in analysis.timings.items()})
         model._kkt_cache = (key, ws, backend)
     else:
         _, ws, backend = cache

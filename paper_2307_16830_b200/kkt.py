@@ -155,6 +155,55 @@ def symbolic_condense(hess_rows, hess_cols, jac_rows, jac_cols, n) -> CondensedS
     return CondensedStructure(mat, h, hr.size, npr.value)
 
 
+class HostAnalysis:
+    """The host half of the symbolic analysis -- condensed pattern, ordering,
+    symbolic factor and front plan -- on a worker thread (the native calls
+    release the GIL), so it overlaps the device-side problem setup and the
+    KKT plan upload of the calling thread.  Pure host work: no CUDA calls."""
+
+    _pool = None
+
+    def __init__(self, model, ordering=None):
+        import concurrent.futures as cf
+        import threading
+
+        if HostAnalysis._pool is None:
+            HostAnalysis._pool = cf.ThreadPoolExecutor(max_workers=4,
+                                                       thread_name_prefix="gn-analysis")
+        self.timings = {}
+        self._cs_ready = threading.Event()
+        self._cs = None
+        self._fut = HostAnalysis._pool.submit(self._run, model, ordering)
+
+    def _run(self, model, ordering):
+        import time
+
+        try:
+            t = time.perf_counter()
+            self._cs = symbolic_condense(model.hess_rows, model.hess_cols, model.jac_rows,
+                                         model.jac_cols, model.n_var)
+            self.timings["condense"] = time.perf_counter() - t
+        finally:
+            self._cs_ready.set()
+        t = time.perf_counter()
+        if ordering is None:
+            ordering = S.amd_order(self._cs.matrix)
+        self.timings["ordering"] = time.perf_counter() - t
+        t = time.perf_counter()
+        sym = S.symbolic_cholesky(self._cs.matrix, ordering)
+        self.timings["symbolic"] = time.perf_counter() - t
+        return sym
+
+    def condensed(self) -> CondensedStructure:
+        self._cs_ready.wait()
+        if self._cs is None:       # condensation failed: raise its error
+            self._fut.result()
+        return self._cs
+
+    def symbolic(self):
+        return self._fut.result()
+
+
 class KKTWorkspace:
     """Device values of the full KKT system at the current iterate (kkt.py:96-221)."""
 
@@ -335,7 +384,8 @@ def residual_norm(pv) -> float:
 class CondensedBackend:
     """Sparse Cholesky of the condensed primal system on the GPU (kkt.py:286-325)."""
 
-    def __init__(self, ws: KKTWorkspace, ordering=None, timings=None, structure=None):
+    def __init__(self, ws: KKTWorkspace, ordering=None, timings=None, structure=None,
+                 symbolic=None):
         import time
 
         tm = timings if timings is not None else {}
@@ -347,13 +397,15 @@ class CondensedBackend:
             tm["condense"] = time.perf_counter() - t
         self.structure = structure
         ws.attach_condensed(self.structure)
-        t = time.perf_counter()
-        if ordering is None:
-            ordering = S.amd_order(self.structure.matrix)
-        tm["ordering"] = time.perf_counter() - t
-        t = time.perf_counter()
-        self.symbolic = S.symbolic_cholesky(self.structure.matrix, ordering)
-        tm["symbolic"] = time.perf_counter() - t
+        if symbolic is None:
+            t = time.perf_counter()
+            if ordering is None:
+                ordering = S.amd_order(self.structure.matrix)
+            tm["ordering"] = time.perf_counter() - t
+            t = time.perf_counter()
+            symbolic = S.symbolic_cholesky(self.structure.matrix, ordering)
+            tm["symbolic"] = time.perf_counter() - t
+        self.symbolic = symbolic
         t = time.perf_counter()
         self.symbolic.handle()
         self.kvals = D.zeros(self.structure.matrix.nnz)
