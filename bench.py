@@ -463,6 +463,20 @@ def main():
                                "frac": ach / peak, "alg_bytes_per_launch": nbytes,
                                "mean_launch_ms": ph["mean_ms"]}
 
+    # the dense supernode part of the refactorisation against the FP64
+    # tensor-core peak measured live on this device (DMMA probe kernel)
+    dmma = _ct.c_double()
+    _lib.check(_lib.lib().gn_measure_dmma_peak(_ct.byref(dmma), D.stream_ptr()))
+    if ref["count"] and dmma.value > 0:
+        tf = info["flops"] / (ref["mean_ms"] * 1e-3) / 1e12
+        secondary["refactor (FP64 flops vs DMMA peak)"] = {
+            "bound": "tensor", "achieved": tf, "peak": dmma.value, "unit": "TFLOP/s",
+            "frac": tf / dmma.value, "flops_per_launch": info["flops"],
+            "peak_kind": "measured (gn_measure_dmma_peak, m8n8k4 f64)",
+            "mean_launch_ms": ref["mean_ms"],
+            "note": "latency-bound: the elimination-tree critical path (dependent fronts and "
+                    "panels), not DMMA or HBM throughput, sets the time"}
+
     # DRAM traffic of one refactorisation from the committed ncu capture of
     # the same kernels (profiles/, tools/profile_round.sh), C3 only
     traffic = None

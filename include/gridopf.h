@@ -181,6 +181,9 @@ int gn_set_concurrency(int k);
  * factor / forward / backward kernels stamp %globaltimer per front (task
  * start, dependencies met, assembled, done).  NULL turns it off. */
 int gn_chol_set_trace(gn_symbolic *sym, int64_t *trace);
+/* Diagnostics: measured FP64 tensor-core (DMMA) throughput of this device
+ * in TFLOP/s (the refactorisation's FLOP-roofline denominator). */
+int gn_measure_dmma_peak(double *tflops, void *stream);
 /* Factor values in the reference CSC layout (l_colptr/l_rowidx). */
 int gn_chol_export_l(gn_symbolic *sym, const double *fronts, double *l_vals, void *stream);
 

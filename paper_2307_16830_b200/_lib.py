@@ -85,6 +85,7 @@ _SIGS = {
     "gn_chol_factor": (c_i32, [P, P, P, P, P]),
     "gn_chol_solve": (c_i32, [P, P, P, P, P, P]),
     "gn_chol_export_l": (c_i32, [P, P, P, P]),
+    "gn_measure_dmma_peak": (c_i32, [P, P]),
     "gn_chol_set_trace": (c_i32, [P, P]),
     "gn_set_concurrency": (c_i32, [c_i32]),
     "gn_symbolic_fronts": (c_i32, [P, P, P, P, P, P, P]),
