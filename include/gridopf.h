@@ -34,6 +34,10 @@ const char *gn_last_error(void);
 int gn_version(void);
 /* kernel launches and plan-upload bytes since the last reset */
 void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset);
+/* Host threads the calling thread's structure analysis (condense, ordering
+ * support, symbolic factor, front plan) may use; <= 0 restores the default.
+ * Thread-local (an analysis worker leaves a core to the launching thread). */
+int gn_set_host_threads(int k);
 
 /* ------------------------------------------------------------------ */
 /* Host structure (CPU; no device needed)                              */

@@ -1,4 +1,6 @@
 // Error reporting and launch/transfer accounting for the C-ABI (gridopf.h).
+#include <omp.h>
+
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -46,6 +48,11 @@ PhaseTimer::~PhaseTimer() {
 
 extern "C" const char *gn_last_error(void) { return gn::g_last_error.c_str(); }
 extern "C" int gn_version(void) { return 1; }
+
+extern "C" int gn_set_host_threads(int k) {
+  omp_set_num_threads(k > 0 ? k : omp_get_num_procs());
+  return 0;
+}
 
 extern "C" void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset) {
   if (launches) *launches = gn::g_launches.load();

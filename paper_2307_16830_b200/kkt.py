@@ -176,8 +176,11 @@ class HostAnalysis:
         self._fut = HostAnalysis._pool.submit(self._run, model, ordering)
 
     def _run(self, model, ordering):
+        import os
         import time
 
+        # leave one core to the launching thread (device setup runs there)
+        L.lib().gn_set_host_threads(max(1, len(os.sched_getaffinity(0)) - 1))
         try:
             t = time.perf_counter()
             self._cs = symbolic_condense(model.hess_rows, model.hess_cols, model.jac_rows,
