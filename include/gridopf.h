@@ -117,6 +117,12 @@ typedef struct gn_symbolic_info_t {
   int64_t n, nnz_a, nnz_l, n_fronts, front_doubles, vec_doubles, max_front, max_cols;
   int64_t n_levels, flops;
 } gn_symbolic_info_t;
+/* condense + (minimum degree when perm is NULL) + symbolic + front plan in
+ * one call; perm_out[n] receives the ordering used.  Same results as the
+ * separate calls. */
+int gn_analyze(int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc, int64_t nj,
+               const int64_t *jr, const int64_t *jc, const int64_t *perm, int64_t *perm_out,
+               gn_condense **cs_out, gn_symbolic **sym_out);
 int gn_symbolic_info(const gn_symbolic *sym, gn_symbolic_info_t *info);
 int gn_symbolic_export(const gn_symbolic *sym, int64_t *parent, int64_t *a_rowptr,
                        int64_t *a_rowcol, int64_t *a_srcslot, int64_t *row_ptr,

@@ -60,6 +60,7 @@ _SIGS = {
     "gn_version": (c_i32, []),
     "gn_stats": (None, [P, P, c_i32]),
     "gn_set_host_threads": (c_i32, [c_i32]),
+    "gn_analyze": (c_i32, [c_i64, c_i64, P, P, c_i64, P, P, P, P, P, P]),
     "gn_canonical_order": (c_i32, [c_i64, c_i32, c_i32, P, P, P, P]),
     "gn_model_create": (c_i32, [P, c_i32, c_i64, c_i64, P]),
     "gn_model_info": (c_i32, [P, P, P, P]),

@@ -10,6 +10,7 @@
 // entries, Jacobian / Hessian COO slots) in the reference's np.add.at
 // order (autodiff.py:57-142): deterministic, no floating-point atomics.
 // A single-CTA kernel reduces the objective.
+#include <new>
 #include <cmath>
 
 #include <cstdio>
@@ -452,8 +453,11 @@ static void upload_model(Model &M) {
   const char *env = std::getenv("GN_AD_INTERPRETER");
   if (!(env && env[0] == '1') && !db.empty()) {
     std::vector<int> pat;
+    PhaseTimer tm_src("upload_model.pattern_source+compile");
     const std::string src = pattern_source(M, pat);
     M.pattern_fn = compile_patterns(src, M.pattern_error);
+    tm_src.~PhaseTimer();
+    new (&tm_src) PhaseTimer("upload_model.pattern_tail");
     if (M.pattern_fn) {
       struct GenBlk { long long cta_begin, R, var_off, par_off, tgt_off, contrib_off, jslot_off; int pattern, pad; };
       std::vector<GenBlk> gb(db.size());

@@ -10,6 +10,10 @@
 //                                            patterns 73-91, L CSC)
 #include <omp.h>
 
+#include <algorithm>
+#include <memory>
+#include <cmath>
+
 #include <cstring>
 #include <new>
 #include <queue>
@@ -131,85 +135,93 @@ static inline uint64_t ckey(int64_t row, int64_t col) {
   return (static_cast<uint64_t>(col) << 32) | static_cast<uint64_t>(row);
 }
 
+// product q of segment g: local index -> (la, lb) with lb <= la, in
+// np.tril_indices order (row-major lower triangle)
+void Condense::product(int64_t q, int64_t g, int64_t &row, int64_t &s1, int64_t &s2) const {
+  const int64_t local = q - seg_poff[g];
+  int64_t la = static_cast<int64_t>((std::sqrt(8.0 * static_cast<double>(local) + 1.0) - 1.0) * 0.5);
+  while ((la + 1) * (la + 2) / 2 <= local) ++la;
+  while (la * (la + 1) / 2 > local) --la;
+  const int64_t lb = local - la * (la + 1) / 2;
+  row = seg_row[g];
+  s1 = seg[g] + la;
+  s2 = seg[g] + lb;
+}
+
+int64_t Condense::product_segment(int64_t q) const {
+  return static_cast<int64_t>(std::upper_bound(seg_poff.begin(), seg_poff.end(), q) - seg_poff.begin()) - 1;
+}
+
 static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc,
                      int64_t nj, const int64_t *jr, const int64_t *jc) {
+  PhaseTimer tm_total("condense.total");
   C.n = n;
   C.nnz_h = nh;
   C.nnz_j = nj;
   GN_REQUIRE(n < (int64_t(1) << 31), "too many variables for 32-bit indices");
+  int bad = 0;
+#pragma omp parallel for reduction(| : bad)
   for (int64_t t = 1; t < nj; ++t)
-    GN_REQUIRE(jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1]),
-               "Jacobian coordinates must be sorted row-major and unique");
-  int64_t np = 0;
-  for (int64_t st = 0; st < nj;) {
-    int64_t en = st;
-    while (en < nj && jr[en] == jr[st]) ++en;
-    np += (en - st) * (en - st + 1) / 2;
-    st = en;
-  }
-  PhaseTimer tm_all("condense");
-  std::vector<int32_t> rows, cols;
-  rows.reserve(nh + n + np);
-  cols.reserve(nh + n + np);
-  for (int64_t t = 0; t < nh; ++t) {
-    GN_REQUIRE(hc[t] <= hr[t], "Hessian entry above the diagonal");
-    GN_REQUIRE(hr[t] >= 0 && hr[t] < n && hc[t] >= 0, "Hessian index out of range");
-    rows.push_back(static_cast<int32_t>(hr[t]));
-    cols.push_back(static_cast<int32_t>(hc[t]));
-  }
-  for (int64_t i = 0; i < n; ++i) {
-    rows.push_back(static_cast<int32_t>(i));
-    cols.push_back(static_cast<int32_t>(i));
-  }
-  C.ata_row.resize(np);
-  C.ata_s1.resize(np);
-  C.ata_s2.resize(np);
+    bad |= !(jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1]));
+  GN_REQUIRE(!bad, "Jacobian coordinates must be sorted row-major and unique");
+#pragma omp parallel for reduction(| : bad)
+  for (int64_t t = 0; t < nh; ++t) bad |= !(hc[t] <= hr[t] && hr[t] >= 0 && hr[t] < n && hc[t] >= 0);
+  GN_REQUIRE(!bad, "Hessian entry out of range or above the diagonal");
   // Jacobian row segments and their product offsets (np.tril_indices order)
-  std::vector<int64_t> seg, poff;
+  C.seg.clear();
+  C.seg_row.clear();
   for (int64_t st = 0; st < nj;) {
     int64_t en = st;
     while (en < nj && jr[en] == jr[st]) ++en;
-    seg.push_back(st);
+    C.seg.push_back(st);
+    C.seg_row.push_back(jr[st]);
     st = en;
   }
-  seg.push_back(nj);
-  poff.assign(seg.size(), 0);
-  for (size_t g = 0; g + 1 < seg.size(); ++g) {
-    const int64_t k = seg[g + 1] - seg[g];
-    poff[g + 1] = poff[g] + k * (k + 1) / 2;
+  const int64_t nseg = static_cast<int64_t>(C.seg.size());
+  C.seg.push_back(nj);
+  C.seg_row.push_back(-1);
+  C.seg_poff.assign(nseg + 1, 0);
+  for (int64_t g = 0; g < nseg; ++g) {
+    const int64_t k = C.seg[g + 1] - C.seg[g];
+    C.seg_poff[g + 1] = C.seg_poff[g] + k * (k + 1) / 2;
   }
+  const int64_t np = C.seg_poff[nseg];
+  C.np = np;
+  GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
+  PhaseTimer tm_all("condense");
   const int64_t base = nh + n;
-  rows.resize(base + np);
-  cols.resize(base + np);
+  std::vector<int32_t> rows(base + np), cols(base + np), pseg(np);
+#pragma omp parallel for
+  for (int64_t t = 0; t < nh; ++t) {
+    rows[t] = static_cast<int32_t>(hr[t]);
+    cols[t] = static_cast<int32_t>(hc[t]);
+  }
+#pragma omp parallel for
+  for (int64_t i = 0; i < n; ++i) rows[nh + i] = cols[nh + i] = static_cast<int32_t>(i);
 #pragma omp parallel for schedule(dynamic, 256)
-  for (int64_t g = 0; g < static_cast<int64_t>(seg.size()) - 1; ++g) {
-    const int64_t st = seg[g], en = seg[g + 1];
-    int64_t q = poff[g];
+  for (int64_t g = 0; g < nseg; ++g) {
+    const int64_t st = C.seg[g], en = C.seg[g + 1];
+    int64_t q = C.seg_poff[g];
     for (int64_t la = 0; la < en - st; ++la)
       for (int64_t lb = 0; lb <= la; ++lb, ++q) {
         rows[base + q] = static_cast<int32_t>(jc[st + la]);
         cols[base + q] = static_cast<int32_t>(jc[st + lb]);
-        C.ata_row[q] = jr[st];
-        C.ata_s1[q] = st + la;
-        C.ata_s2[q] = st + lb;
+        pseg[q] = static_cast<int32_t>(g);
       }
   }
-  std::vector<int64_t> slot, bptr;
+  std::vector<int64_t> bptr;
   std::vector<int32_t> bucket;
   {
     PhaseTimer tm("condense.csc_from_coords");
-    csc_from_coords(n, rows, cols, C.indptr, C.indices, slot, &bucket, &bptr);
+    csc_from_coords(n, rows, cols, C.indptr, C.indices, C.slot, &bucket, &bptr);
   }
-  C.w_map.assign(slot.begin(), slot.begin() + nh);
-  C.diag_map.assign(slot.begin() + nh, slot.begin() + nh + n);
-  C.ata_map.assign(slot.begin() + nh + n, slot.end());
   // assembly plan: the A^T A products grouped by K slot, ascending product
   // index inside a slot (the summation order of kkt.py:243-283).  The column
   // buckets already hold every coordinate of a column in input order, and a
   // slot belongs to one column, so columns are processed independently.
   PhaseTimer tm_plan("condense.assembly_plan");
   const int64_t nk = C.indptr[n];
-  GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
+  const std::vector<int64_t> &slot = C.slot;
   C.k_ptr.assign(nk + 1, 0);
   C.k_row.resize(np);
   C.k_s1.resize(np);
@@ -230,10 +242,12 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
         const int64_t t = bucket[q];
         if (t < base) continue;
         const int64_t p = t - base;
+        int64_t row, s1, s2;
+        C.product(p, pseg[p], row, s1, s2);
         const int32_t d = fill[slot[t] - s0]++;
-        C.k_row[d] = static_cast<int32_t>(C.ata_row[p]);
-        C.k_s1[d] = static_cast<int32_t>(C.ata_s1[p]);
-        C.k_s2[d] = static_cast<int32_t>(C.ata_s2[p]);
+        C.k_row[d] = static_cast<int32_t>(row);
+        C.k_s1[d] = static_cast<int32_t>(s1);
+        C.k_s2[d] = static_cast<int32_t>(s2);
       }
     }
   }
@@ -425,21 +439,76 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
     }
   }
   tm_perm.~PhaseTimer();
-  new (&tm_perm) PhaseTimer("symbolic.L_transpose");
-  // L in CSC, diagonal first, rows increasing (cholesky.py:118-131): a
-  // stable bucketing of the row-pattern entries by column
-  const int64_t nrc = S.row_ptr[n];
+  new (&tm_perm) PhaseTimer("symbolic.col_counts");
+  // column counts of L (diagonal + row-pattern entries per column); the row
+  // indices themselves are only built for exports (ensure_l_csc)
+  {
+    const int nt = omp_get_max_threads();
+    std::vector<std::vector<int32_t>> h(nt);
+    const int64_t nrc = S.row_ptr[n];
+#pragma omp parallel num_threads(nt)
+    {
+      std::vector<int32_t> &mine = h[omp_get_thread_num()];
+      mine.assign(n, 0);
+#pragma omp for schedule(static)
+      for (int64_t t = 0; t < nrc; ++t) mine[S.row_cols[t]]++;
+    }
+    S.l_colptr.assign(n + 1, 0);
+    std::vector<int64_t> cnt(n);
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < n; ++j) {
+      int64_t c = 1;
+      for (int t = 0; t < nt; ++t) c += h[t][j];
+      cnt[j] = c;
+    }
+    for (int64_t j = 0; j < n; ++j) S.l_colptr[j + 1] = S.l_colptr[j] + cnt[j];
+    S.nnz_l = S.l_colptr[n];
+  }
+}
+
+// L in CSC, diagonal first, rows increasing (cholesky.py:118-131): a stable
+// bucketing of the row-pattern entries by column.  Export only.
+void Symbolic::ensure_l_csc() {
+  std::lock_guard<std::mutex> g(lazy_mu);
+  if (static_cast<int64_t>(l_rowidx.size()) == nnz_l) return;
+  const int64_t nrc = row_ptr[n];
   std::vector<int32_t> rowof(nrc);
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t k = 0; k < n; ++k)
-    for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) rowof[t] = static_cast<int32_t>(k);
+    for (int64_t t = row_ptr[k]; t < row_ptr[k + 1]; ++t) rowof[t] = static_cast<int32_t>(k);
   std::vector<int64_t> cptr;
-  S.l_rowidx.assign(nrc + n, 0);
-  par_bucket(n, nrc, [&](int64_t t) { return S.row_cols[t]; },
-             [&](int64_t t, int64_t d) { S.l_rowidx[d + S.row_cols[t] + 1] = rowof[t]; }, cptr);
-  S.l_colptr.resize(n + 1);
-  for (int64_t j = 0; j <= n; ++j) S.l_colptr[j] = cptr[j] + j;
-  for (int64_t j = 0; j < n; ++j) S.l_rowidx[S.l_colptr[j]] = j;
+  l_rowidx.assign(nrc + n, 0);
+  par_bucket(n, nrc, [&](int64_t t) { return row_cols[t]; },
+             [&](int64_t t, int64_t d) { l_rowidx[d + row_cols[t] + 1] = rowof[t]; }, cptr);
+  for (int64_t j = 0; j < n; ++j) l_rowidx[l_colptr[j]] = j;
+}
+
+// reference L slot -> offset in the front storage.  Export only.
+void Symbolic::ensure_l_export() {
+  ensure_l_csc();
+  std::lock_guard<std::mutex> g(lazy_mu);
+  if (static_cast<int64_t>(l_export.size()) == nnz_l) return;
+  l_export.assign(nnz_l, 0);
+  int missing = 0;
+#pragma omp parallel reduction(| : missing)
+  {
+    std::vector<int32_t> pos(n, -1);
+#pragma omp for schedule(dynamic, 64)
+    for (int64_t J = 0; J < nf; ++J) {
+      const int64_t r0 = f_rows_off[J], r1 = f_rows_off[J + 1], sJ = f_nrows[J];
+      for (int64_t q = r0; q < r1; ++q) pos[f_rows[q]] = static_cast<int32_t>(q - r0);
+      for (int64_t j = f_first[J]; j < f_first[J] + f_ncols[J]; ++j) {
+        const int64_t base = f_off[J] + (j - f_first[J]) * sJ;
+        for (int64_t p = l_colptr[j]; p < l_colptr[j + 1]; ++p) {
+          const int32_t v = pos[l_rowidx[p]];
+          missing |= v < 0;
+          l_export[p] = base + (v < 0 ? 0 : v);
+        }
+      }
+      for (int64_t q = r0; q < r1; ++q) pos[f_rows[q]] = -1;
+    }
+  }
+  GN_REQUIRE(!missing, "row missing from front structure");
 }
 
 // ------------------------------------------------------------ front plan
@@ -486,29 +555,53 @@ static void front_plan(Symbolic &S) {
   S.nf = nf;
   for (int64_t J = 0; J < nf; ++J)
     for (int64_t c = S.f_first[J]; c < S.f_first[J] + S.f_ncols[J]; ++c) snode_of[c] = static_cast<int32_t>(J);
-  // rows, sizes, offsets
+  // rows, sizes, offsets.  Front rows = its columns, then the structure of
+  // its last column below the diagonal: the row-pattern entries (k, l) with
+  // l a last column, bucketed by front in ascending k.
   S.f_nrows.resize(nf);
   S.f_parent.assign(nf, -1);
   S.f_rows_off.assign(nf + 1, 0);
-  S.f_rows.clear();
   S.f_off.assign(nf + 1, 0);
   S.f_voff.assign(nf + 1, 0);
   S.max_front = S.max_cols = 0;
   S.flops = 0;
+  std::vector<int32_t> last_of(n, -1);
   for (int64_t J = 0; J < nf; ++J) {
     int64_t first = S.f_first[J], w = S.f_ncols[J], l = first + w - 1;
-    for (int64_t c = first; c <= l; ++c) S.f_rows.push_back(static_cast<int32_t>(c));
-    for (int64_t p = S.l_colptr[l] + 1; p < S.l_colptr[l + 1]; ++p)
-      S.f_rows.push_back(static_cast<int32_t>(S.l_rowidx[p]));
+    last_of[l] = static_cast<int32_t>(J);
     int64_t s = w + cc[l] - 1;
     S.f_nrows[J] = static_cast<int32_t>(s);
-    S.f_rows_off[J + 1] = static_cast<int64_t>(S.f_rows.size());
+    S.f_rows_off[J + 1] = S.f_rows_off[J] + s;
     S.f_off[J + 1] = S.f_off[J] + s * s;
     S.f_voff[J + 1] = S.f_voff[J] + s;
     S.max_front = std::max(S.max_front, s);
     S.max_cols = std::max(S.max_cols, w);
     if (S.parent[l] != -1) S.f_parent[J] = snode_of[S.parent[l]];
     for (int64_t c = 0; c < w; ++c) S.flops += (s - c - 1) * (s - c - 1) + 2 * (s - c);
+  }
+  {
+    PhaseTimer tm_rows("front_plan.rows");
+    const int64_t nrc = S.row_ptr[n];
+    std::vector<int32_t> rowof(nrc);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t k = 0; k < n; ++k)
+      for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) rowof[t] = static_cast<int32_t>(k);
+    std::vector<int64_t> sptr;
+    S.f_rows.assign(S.f_rows_off[nf], 0);
+    std::vector<int32_t> srow(S.f_rows_off[nf]);   // >= the struct entries
+    par_bucket(nf + 1, nrc,
+               [&](int64_t t) { const int32_t J = last_of[S.row_cols[t]]; return J >= 0 ? J : nf; },
+               [&](int64_t t, int64_t d) {
+                 if (last_of[S.row_cols[t]] >= 0) srow[d] = rowof[t];
+               },
+               sptr);
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t J = 0; J < nf; ++J) {
+      const int64_t o = S.f_rows_off[J], w = S.f_ncols[J];
+      GN_REQUIRE(sptr[J + 1] - sptr[J] == S.f_nrows[J] - w, "front structure mismatch");
+      for (int64_t c = 0; c < w; ++c) S.f_rows[o + c] = static_cast<int32_t>(S.f_first[J] + c);
+      for (int64_t q = sptr[J]; q < sptr[J + 1]; ++q) S.f_rows[o + w + (q - sptr[J])] = srow[q];
+    }
   }
   S.dinv_off = S.f_off[nf];                // 1 / L[k][k] per column, after the fronts
   S.front_doubles = S.f_off[nf] + n;
@@ -546,7 +639,6 @@ static void front_plan(Symbolic &S) {
   S.relmap.assign(S.f_relmap_off[nf], 0);
   S.a_kslot.assign(na, 0);
   S.a_fpos.assign(na, 0);
-  S.l_export.assign(S.l_rowidx.size(), 0);
   // local row positions through a dense per-thread position map filled per
   // front (O(1) lookups); every front writes disjoint ranges (its own A
   // entries, its columns of L, its children's relmaps)
@@ -574,11 +666,6 @@ static void front_plan(Symbolic &S) {
         const int64_t t = a_t[q], j = S.a_rowcol[t];
         S.a_kslot[q] = S.a_srcslot[t];
         S.a_fpos[q] = S.f_off[J] + (j - S.f_first[J]) * sJ + local(arow[t]);
-      }
-      for (int64_t j = S.f_first[J]; j < S.f_first[J] + S.f_ncols[J]; ++j) {   // reference L layout
-        const int64_t base = S.f_off[J] + (j - S.f_first[J]) * sJ;
-        for (int64_t p = S.l_colptr[j]; p < S.l_colptr[j + 1]; ++p)
-          S.l_export[p] = base + local(S.l_rowidx[p]);
       }
       for (int64_t q = r0; q < r1; ++q) pos[S.f_rows[q]] = -1;
     }
@@ -657,7 +744,7 @@ extern "C" int gn_condense_create(int64_t n, int64_t nh, const int64_t *hr, cons
 extern "C" int gn_condense_info(const gn_condense *C, int64_t *nnz_k, int64_t *np) {
   return guarded([&] {
     if (nnz_k) *nnz_k = static_cast<int64_t>(C->indices.size());
-    if (np) *np = static_cast<int64_t>(C->ata_map.size());
+    if (np) *np = C->np;
   });
 }
 
@@ -672,12 +759,22 @@ extern "C" int gn_condense_export(const gn_condense *C, int64_t *indptr, int64_t
   return guarded([&] {
     copy_out(indptr, C->indptr);
     copy_out(indices, C->indices);
-    copy_out(w_map, C->w_map);
-    copy_out(diag_map, C->diag_map);
-    copy_out(ata_map, C->ata_map);
-    copy_out(ata_row, C->ata_row);
-    copy_out(ata_s1, C->ata_s1);
-    copy_out(ata_s2, C->ata_s2);
+    const int64_t nh = C->nnz_h, n = C->n, np = C->np;
+    if (w_map) std::memcpy(w_map, C->slot.data(), sizeof(int64_t) * nh);
+    if (diag_map) std::memcpy(diag_map, C->slot.data() + nh, sizeof(int64_t) * n);
+    if (ata_map) std::memcpy(ata_map, C->slot.data() + nh + n, sizeof(int64_t) * np);
+    if (ata_row || ata_s1 || ata_s2) {
+      const int64_t nseg = static_cast<int64_t>(C->seg.size()) - 1;
+#pragma omp parallel for schedule(dynamic, 256)
+      for (int64_t g = 0; g < nseg; ++g)
+        for (int64_t q = C->seg_poff[g]; q < C->seg_poff[g + 1]; ++q) {
+          int64_t row, s1, s2;
+          C->product(q, g, row, s1, s2);
+          if (ata_row) ata_row[q] = row;
+          if (ata_s1) ata_s1[q] = s1;
+          if (ata_s2) ata_s2[q] = s2;
+        }
+    }
   });
 }
 
@@ -724,11 +821,36 @@ extern "C" int gn_symbolic_create(int64_t n, const int64_t *indptr, const int64_
   });
 }
 
+// The whole host analysis of one sparsity pattern in one call (condensed
+// pattern, minimum degree unless `perm` is given, symbolic factor, front
+// plan): a caller running it on a worker thread holds no interpreter lock
+// in between.  `perm_out` (n) receives the ordering used.
+extern "C" int gn_analyze(int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc, int64_t nj,
+                          const int64_t *jr, const int64_t *jc, const int64_t *perm, int64_t *perm_out,
+                          gn_condense **cs_out, gn_symbolic **sym_out) {
+  return guarded([&] {
+    GN_REQUIRE(n < (int64_t(1) << 31), "matrix too large for 32-bit device indices");
+    std::unique_ptr<gn_condense> C(new gn_condense());
+    condense(*C, n, nh, hr, hc, nj, jr, jc);
+    if (perm) {
+      std::memcpy(perm_out, perm, sizeof(int64_t) * n);
+    } else {
+      PhaseTimer tm("min_degree");
+      min_degree(n, C->indptr.data(), C->indices.data(), perm_out);
+    }
+    std::unique_ptr<gn_symbolic> S(new gn_symbolic());
+    symbolic(*S, n, C->indptr.data(), C->indices.data(), perm_out);
+    if (n > 0) front_plan(*S);
+    *cs_out = C.release();
+    *sym_out = S.release();
+  });
+}
+
 extern "C" int gn_symbolic_info(const gn_symbolic *S, gn_symbolic_info_t *info) {
   return guarded([&] {
     info->n = S->n;
     info->nnz_a = S->nnz_a;
-    info->nnz_l = static_cast<int64_t>(S->l_rowidx.size());
+    info->nnz_l = S->nnz_l;
     info->n_fronts = S->nf;
     info->front_doubles = S->front_doubles;
     info->vec_doubles = S->vec_doubles;
@@ -750,7 +872,10 @@ extern "C" int gn_symbolic_export(const gn_symbolic *S, int64_t *parent, int64_t
     copy_out(row_ptr, S->row_ptr);
     copy_out(row_cols, S->row_cols);
     copy_out(l_colptr, S->l_colptr);
-    copy_out(l_rowidx, S->l_rowidx);
+    if (l_rowidx) {
+      const_cast<Symbolic *>(static_cast<const Symbolic *>(S))->ensure_l_csc();
+      copy_out(l_rowidx, S->l_rowidx);
+    }
   });
 }
 

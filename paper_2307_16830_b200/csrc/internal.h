@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/gridopf.h"
@@ -136,10 +137,22 @@ struct Model {
 
 // --------------------------------------------------------- condensation
 struct Condense {
-  int64_t n = 0, nnz_h = 0, nnz_j = 0;
+  int64_t n = 0, nnz_h = 0, nnz_j = 0, np = 0;
   std::vector<int64_t> indptr, indices;
-  std::vector<int64_t> w_map, diag_map, ata_map, ata_row, ata_s1, ata_s2;
+  // K slot of every coordinate, in input order: the nnz_h W entries
+  // (w_map), the n diagonal entries (diag_map), the np A^T A products
+  // (ata_map) -- the reference's three maps as slices of one array
+  std::vector<int64_t> slot;
+  // Jacobian row segments: start, product offset (np.tril_indices order),
+  // constraint row; one trailing entry
+  std::vector<int64_t> seg, seg_poff, seg_row;
   std::vector<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
+  int64_t w_map(int64_t p) const { return slot[p]; }
+  int64_t diag_map(int64_t i) const { return slot[nnz_h + i]; }
+  int64_t ata_map(int64_t q) const { return slot[nnz_h + n + q]; }
+  // product q -> (Jacobian row, first factor slot, second factor slot)
+  void product(int64_t q, int64_t g, int64_t &row, int64_t &s1, int64_t &s2) const;
+  int64_t product_segment(int64_t q) const;
 };
 
 // ------------------------------------------------------- symbolic factor
@@ -158,9 +171,15 @@ struct alignas(16) FrontMeta {
 };
 
 struct Symbolic {
-  int64_t n = 0, nnz_a = 0;
+  int64_t n = 0, nnz_a = 0, nnz_l = 0;
   std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, row_cols,
-      l_colptr, l_rowidx;
+      l_colptr;
+  // the reference L row indices (CSC) and the L -> front map are only needed
+  // for exports: built on first use (ensure_l_csc / ensure_l_export)
+  std::vector<int64_t> l_rowidx;
+  void ensure_l_csc();
+  void ensure_l_export();
+  std::mutex lazy_mu;
   // ---- supernodal front plan (internal order = reference elimination order)
   int64_t nf = 0;                              // number of fronts
   std::vector<int32_t> f_first, f_ncols, f_nrows, f_parent;

@@ -388,15 +388,15 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
   if (cs) {
     GN_REQUIRE(cs->n == n && cs->nnz_h == nh && cs->nnz_j == nj, "condensed structure mismatch");
     const int64_t nk = static_cast<int64_t>(cs->indices.size());
-    const int64_t np = static_cast<int64_t>(cs->ata_map.size());
+    const int64_t np = cs->np;
     K.nk = nk;
     K.np = np;
     std::vector<int32_t> kw(nk, -1), kd(nk, -1);
     for (int64_t p = 0; p < nh; ++p) {
-      GN_REQUIRE(kw[cs->w_map[p]] == -1, "duplicate W entry in a K slot");
-      kw[cs->w_map[p]] = static_cast<int32_t>(p);
+      GN_REQUIRE(kw[cs->w_map(p)] == -1, "duplicate W entry in a K slot");
+      kw[cs->w_map(p)] = static_cast<int32_t>(p);
     }
-    for (int64_t i = 0; i < n; ++i) kd[cs->diag_map[i]] = static_cast<int32_t>(i);
+    for (int64_t i = 0; i < n; ++i) kd[cs->diag_map(i)] = static_cast<int32_t>(i);
     K.d.k_ptr = dev_upload(cs->k_ptr);
     K.d.k_row = dev_upload(cs->k_row);
     K.d.k_s1 = dev_upload(cs->k_s1);

@@ -162,18 +162,44 @@ class HostAnalysis:
     KKT plan upload of the calling thread.  Pure host work: no CUDA calls."""
 
     _pool = None
+    # While an analysis runs, the interpreter's thread switch interval is cut
+    # to 0.1 ms: the worker needs the GIL for a moment between its native
+    # calls, and the launching thread is busy in Python (device setup), so
+    # the default 5 ms interval would stall the worker at every hand-over.
+    _active = 0
+    _saved_interval = None
+    _lock = None
 
     def __init__(self, model, ordering=None):
         import concurrent.futures as cf
+        import sys
         import threading
 
         if HostAnalysis._pool is None:
             HostAnalysis._pool = cf.ThreadPoolExecutor(max_workers=4,
                                                        thread_name_prefix="gn-analysis")
+            HostAnalysis._lock = threading.Lock()
+        with HostAnalysis._lock:
+            if HostAnalysis._active == 0:
+                HostAnalysis._saved_interval = sys.getswitchinterval()
+                sys.setswitchinterval(min(1e-4, HostAnalysis._saved_interval))
+            HostAnalysis._active += 1
+        self._released = False
         self.timings = {}
         self._cs_ready = threading.Event()
         self._cs = None
         self._fut = HostAnalysis._pool.submit(self._run, model, ordering)
+
+    def _release(self):
+        import sys
+
+        if self._released:
+            return
+        self._released = True
+        with HostAnalysis._lock:
+            HostAnalysis._active -= 1
+            if HostAnalysis._active == 0 and HostAnalysis._saved_interval is not None:
+                sys.setswitchinterval(HostAnalysis._saved_interval)
 
     def _run(self, model, ordering):
         import os
@@ -204,7 +230,18 @@ class HostAnalysis:
         return self._cs
 
     def symbolic(self):
-        return self._fut.result()
+        try:
+            return self._fut.result()
+        finally:
+            self._release()
+
+    def __del__(self):
+        try:
+            if not self._released:
+                self._fut.result()
+                self._release()
+        except Exception:
+            pass
 
 
 class KKTWorkspace:
