@@ -115,3 +115,37 @@ def test_refactor_bitwise_large():
     a = S.factorize(sym, m.values).values
     b = S.factorize(sym, m.values).values
     assert np.array_equal(a, b)
+
+
+def test_dense_front_nb16_three_rows_per_thread():
+    m, _ = dense_spd(700, 7)   # 16-column panels, 3 rows per thread, two panel buffers
+    check_against_oracle(m, np.arange(700))
+
+
+@pytest.mark.parametrize("n", [200, 330])
+def test_double_buffered_panels_bitwise_equal_single_buffer(n, monkeypatch):
+    """The next panel built in shared memory by the strip update (two panel
+    buffers) is bitwise the one reloaded from the front (one buffer)."""
+    m, _ = dense_spd(n, n + 1)
+    sym = S.symbolic_cholesky(m, np.arange(n))
+    two = S.factorize(sym, m.values).values
+    monkeypatch.setenv("GN_SINGLE_PANEL_BUFFER", "1")
+    one = S.factorize(sym, m.values).values
+    assert np.array_equal(one, two)
+    g = grid_laplacian(60, seed=5)   # CTA-per-front kernel below the top fronts
+    gs = S.symbolic_cholesky(g, S.amd_order(g))
+    one = S.factorize(gs, g.values).values
+    monkeypatch.delenv("GN_SINGLE_PANEL_BUFFER")
+    assert np.array_equal(one, S.factorize(gs, g.values).values)
+
+
+def test_measured_dmma_peak_is_plausible():
+    import ctypes
+
+    import torch
+
+    from paper_2307_16830_b200 import _lib as L
+
+    tf = ctypes.c_double()
+    L.check(L.lib().gn_measure_dmma_peak(ctypes.byref(tf), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert 5.0 < tf.value < 200.0   # B200 FP64 tensor cores: ~37 TFLOP/s

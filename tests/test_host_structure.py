@@ -165,3 +165,55 @@ def test_min_degree_matches_shipped_reference_at_2k_buses():
     cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
     assert cs.matrix.indices.size == int(g["nnz_k"])
     np.testing.assert_array_equal(sparse.amd_order(cs.matrix), g["perm"].astype(np.int64))
+
+
+@pytest.mark.parametrize("tiles", [1, 16])
+@pytest.mark.parametrize("inject", [False, True])
+def test_analyze_single_call_matches_separate_calls(tiles, inject):
+    """gn_analyze (condense + ordering + symbolic + front plan in one native
+    call, as the analysis worker can use it) equals the separate entry points."""
+    import ctypes
+
+    from paper_2307_16830_b200 import _lib as L
+
+    m = build_acopf(parse_matpower(tiled_case(tiles))).model
+    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
+    perm = sparse.amd_order(cs.matrix)
+    sym = sparse.symbolic_cholesky(cs.matrix, perm)
+    hr, hc, jr, jc = (L.i64(a) for a in (m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols))
+    perm_out = np.empty(m.n_var, np.int64)
+    hcs, hsym = ctypes.c_void_p(), ctypes.c_void_p()
+    pin = L.i64(perm) if inject else None
+    L.check(L.lib().gn_analyze(m.n_var, hr.size, L.ptr(hr), L.ptr(hc), jr.size, L.ptr(jr), L.ptr(jc),
+                               None if pin is None else L.ptr(pin), L.ptr(perm_out),
+                               ctypes.byref(hcs), ctypes.byref(hsym)))
+    try:
+        np.testing.assert_array_equal(perm_out, perm)
+        nk, npr = ctypes.c_int64(), ctypes.c_int64()
+        L.check(L.lib().gn_condense_info(hcs, ctypes.byref(nk), ctypes.byref(npr)))
+        assert (nk.value, npr.value) == (cs.matrix.nnz, cs._np)
+        maps = {k: np.empty(n, np.int64) for k, n in (
+            ("indptr", m.n_var + 1), ("indices", nk.value), ("w_map", hr.size), ("diag_map", m.n_var),
+            ("ata_map", npr.value), ("ata_row", npr.value), ("ata_s1", npr.value), ("ata_s2", npr.value))}
+        L.check(L.lib().gn_condense_export(hcs, *(L.ptr(maps[k]) for k in (
+            "indptr", "indices", "w_map", "diag_map", "ata_map", "ata_row", "ata_s1", "ata_s2"))))
+        np.testing.assert_array_equal(maps["indptr"], cs.matrix.indptr)
+        np.testing.assert_array_equal(maps["indices"], cs.matrix.indices)
+        for f in ("w_map", "diag_map", "ata_map", "ata_row", "ata_s1", "ata_s2"):
+            np.testing.assert_array_equal(maps[f], getattr(cs, f))
+        info = L.SymbolicInfo()
+        L.check(L.lib().gn_symbolic_info(hsym, ctypes.byref(info)))
+        assert {f: getattr(info, f) for f, _ in L.SymbolicInfo._fields_} == sym.info
+        nf = sym.info["n_fronts"]
+        fa = {k: np.empty(nf, np.int32) for k in ("first", "ncols", "nrows", "parent", "order")}
+        nsm = ctypes.c_int64()
+        L.check(L.lib().gn_symbolic_fronts(hsym, *(L.ptr(fa[k]) for k in
+                                                   ("first", "ncols", "nrows", "parent", "order")),
+                                           ctypes.byref(nsm)))
+        ref = sparse.front_plan(sym)
+        for k in ("first", "ncols", "nrows", "parent", "order"):
+            np.testing.assert_array_equal(fa[k], ref[k])
+        assert nsm.value == ref["nf_small"]
+    finally:
+        L.lib().gn_condense_destroy(hcs)
+        L.lib().gn_symbolic_destroy(hsym)
