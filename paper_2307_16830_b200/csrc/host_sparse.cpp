@@ -215,42 +215,57 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
     PhaseTimer tm("condense.csc_from_coords");
     csc_from_coords(n, rows, cols, C.indptr, C.indices, C.slot, &bucket, &bptr);
   }
-  // assembly plan: the A^T A products grouped by K slot, ascending product
-  // index inside a slot (the summation order of kkt.py:243-283).  The column
-  // buckets already hold every coordinate of a column in input order, and a
-  // slot belongs to one column, so columns are processed independently.
+  // the assembly plan is built on first use (gn_kkt_create, usually on the
+  // launching thread while the analysis worker runs the symbolic factor)
+  C.plan_bucket = std::move(bucket);
+  C.plan_bptr = std::move(bptr);
+  C.plan_pseg = std::move(pseg);
+}
+
+// assembly plan: the A^T A products grouped by K slot, ascending product
+// index inside a slot (the summation order of kkt.py:243-283).  The column
+// buckets already hold every coordinate of a column in input order, and a
+// slot belongs to one column, so columns are processed independently.
+void Condense::ensure_assembly_plan() {
+  std::lock_guard<std::mutex> g(plan_mu);
+  if (plan_built) return;
   PhaseTimer tm_plan("condense.assembly_plan");
-  const int64_t nk = C.indptr[n];
-  const std::vector<int64_t> &slot = C.slot;
-  C.k_ptr.assign(nk + 1, 0);
-  C.k_row.resize(np);
-  C.k_s1.resize(np);
-  C.k_s2.resize(np);
+  const int64_t nk = indptr[n], base = nnz_h + n;
+  const std::vector<int32_t> &bucket = plan_bucket, &pseg = plan_pseg;
+  const std::vector<int64_t> &bptr = plan_bptr;
+  k_ptr.assign(nk + 1, 0);
+  k_row.resize(np);
+  k_s1.resize(np);
+  k_s2.resize(np);
 #pragma omp parallel for schedule(dynamic, 512)
   for (int64_t c = 0; c < n; ++c)
     for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q)
-      if (bucket[q] >= base) C.k_ptr[slot[bucket[q]] + 1]++;
-  for (int64_t s = 0; s < nk; ++s) C.k_ptr[s + 1] += C.k_ptr[s];
+      if (bucket[q] >= base) k_ptr[slot[bucket[q]] + 1]++;
+  for (int64_t s = 0; s < nk; ++s) k_ptr[s + 1] += k_ptr[s];
 #pragma omp parallel
   {
     std::vector<int32_t> fill;
 #pragma omp for schedule(dynamic, 512)
     for (int64_t c = 0; c < n; ++c) {
-      const int64_t s0 = C.indptr[c];
-      fill.assign(C.k_ptr.begin() + s0, C.k_ptr.begin() + C.indptr[c + 1]);
+      const int64_t s0 = indptr[c];
+      fill.assign(k_ptr.begin() + s0, k_ptr.begin() + indptr[c + 1]);
       for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
         const int64_t t = bucket[q];
         if (t < base) continue;
         const int64_t p = t - base;
         int64_t row, s1, s2;
-        C.product(p, pseg[p], row, s1, s2);
+        product(p, pseg[p], row, s1, s2);
         const int32_t d = fill[slot[t] - s0]++;
-        C.k_row[d] = static_cast<int32_t>(row);
-        C.k_s1[d] = static_cast<int32_t>(s1);
-        C.k_s2[d] = static_cast<int32_t>(s2);
+        k_row[d] = static_cast<int32_t>(row);
+        k_s1[d] = static_cast<int32_t>(s1);
+        k_s2[d] = static_cast<int32_t>(s2);
       }
     }
   }
+  std::vector<int32_t>().swap(plan_bucket);
+  std::vector<int64_t>().swap(plan_bptr);
+  std::vector<int32_t>().swap(plan_pseg);
+  plan_built = true;
 }
 
 // ------------------------------------------------------------ ordering

@@ -147,6 +147,12 @@ struct Condense {
   // constraint row; one trailing entry
   std::vector<int64_t> seg, seg_poff, seg_row;
   std::vector<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
+  // inputs of the assembly plan until it is built (ensure_assembly_plan)
+  std::vector<int32_t> plan_bucket, plan_pseg;
+  std::vector<int64_t> plan_bptr;
+  bool plan_built = false;
+  std::mutex plan_mu;
+  void ensure_assembly_plan();
   int64_t w_map(int64_t p) const { return slot[p]; }
   int64_t diag_map(int64_t i) const { return slot[nnz_h + i]; }
   int64_t ata_map(int64_t q) const { return slot[nnz_h + n + q]; }

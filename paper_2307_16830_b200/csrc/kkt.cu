@@ -387,6 +387,7 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
   K.d.dvec = dev_alloc<double>(m > 0 ? m : 1);
   if (cs) {
     GN_REQUIRE(cs->n == n && cs->nnz_h == nh && cs->nnz_j == nj, "condensed structure mismatch");
+    const_cast<Condense *>(cs)->ensure_assembly_plan();
     const int64_t nk = static_cast<int64_t>(cs->indices.size());
     const int64_t np = cs->np;
     K.nk = nk;
