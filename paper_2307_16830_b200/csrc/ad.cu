@@ -290,7 +290,18 @@ __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contr
   const GatherSeg &G = ga.seg[s];
   int64_t o = t - ga.begin[s];
   double acc = 0.0;
-  for (int64_t p = G.ptr[o]; p < G.ptr[o + 1]; ++p) acc = __dadd_rn(acc, contrib[G.src[p]]);
+  const int64_t p1 = G.ptr[o + 1];
+  for (int64_t p = G.ptr[o]; p < p1; p += 4) {   // four terms' loads in flight, same order
+    int64_t src[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) src[u] = p + u < p1 ? G.src[p + u] : 0;
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p + u < p1 ? contrib[src[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p + u < p1) acc = __dadd_rn(acc, v[u]);
+  }
   if (!isfinite(acc)) atomicOr(flags, G.bit);
   double sc = 1.0;
   if (G.mode == 1) sc = G.scalar;

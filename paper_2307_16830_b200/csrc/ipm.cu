@@ -8,6 +8,7 @@
 // block that the driver reads back in one copy.
 #include <cmath>
 
+#include "gather.cuh"
 #include "reduce.cuh"
 
 namespace gn {
@@ -49,8 +50,8 @@ prep_x_kernel(int64_t n, const int64_t *atptr, const int32_t *atp, const int32_t
     v.dxl[j] = wl;
     v.dxu[j] = wu;
     v.sx[j] = __dadd_rn(__dmul_rn(zl, inv0(wl)), __dmul_rn(zu, inv0(wu)));
-    double aty = 0.0;
-    for (int64_t t = atptr[j]; t < atptr[j + 1]; ++t) aty += v.jac[atp[t]] * v.y[atrow[t]];
+    const double aty = gather_dot_fma(atptr[j], atptr[j + 1], v.jac, [&](int64_t t) { return atp[t]; }, v.y,
+                                      [&](int64_t t) { return atrow[t]; });
     const double dx = ((v.grad[j] + aty) - zl) + zu;
     v.dual_x[j] = dx;
     acc[0] = red_combine(RED_MAX, acc[0], fabs(dx));

@@ -8,6 +8,7 @@
 // bitwise equal to the reference given equal inputs.
 #include <cmath>
 
+#include "gather.cuh"
 #include "reduce.cuh"
 
 namespace gn {
@@ -66,33 +67,48 @@ __global__ void sigma_kernel(int64_t len, const double *dl, const double *du, co
   if (i < len) out[i] = __dadd_rn(__dmul_rn(zl[i], inv_or_zero(dl[i])), __dmul_rn(zu[i], inv_or_zero(du[i])));
 }
 
+// sum_t a[ia[t]] * b[ib[t]] over t in [t0, t1) in double-double, accumulated
+// in ascending t (the order of the plain loop) with the index and value
+// loads of four terms issued before their sequential accumulation: the
+// gathers' L2 latency overlaps instead of being paid per term
+template <class IA, class IB>
+__device__ __forceinline__ dd dd_gather_dot(int64_t t0, int64_t t1, const double *__restrict__ a, IA ia,
+                                            const double *__restrict__ b, IB ib) {
+  dd acc = {0.0, 0.0};
+  for (int64_t t = t0; t < t1; t += 4) {   // predicated chunks: no serial remainder loop
+    double va[4], vb[4];
+    gather4(t, t1, a, ia, b, ib, va, vb);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t + u < t1) acc = dd_add(acc, dd_prod(va[u], vb[u]));
+  }
+  return acc;
+}
+
 // W v from the lower triangle: first every entry's row contribution, then
 // the mirrored off-diagonal contributions (kkt.py:132-138)
 __global__ void w_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *wp, const int32_t *wj,
                                 const double *w, const double *v, double *out) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= n) return;
-  double acc = 0.0;
-  for (int64_t t = ptr[i]; t < ptr[i + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(w[wp[t]], v[wj[t]]));
-  out[i] = acc;
+  out[i] = gather_dot(ptr[i], ptr[i + 1], w, [&](int64_t t) { return wp[t]; }, v,
+                      [&](int64_t t) { return wj[t]; });
 }
 
 __global__ void a_matvec_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, const double *a,
                                 const double *v, double *out) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= m) return;
-  double acc = 0.0;
-  for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) acc = __dadd_rn(acc, __dmul_rn(a[p], v[col[p]]));
-  out[i] = acc;
+  out[i] = gather_dot(rowptr[i], rowptr[i + 1], a, [](int64_t p) { return p; }, v,
+                      [&](int64_t p) { return col[p]; });
 }
 
 __global__ void at_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *pp, const int32_t *row,
                                  const double *a, const double *u, double *out) {
   int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (j >= n) return;
-  double acc = 0.0;
-  for (int64_t t = ptr[j]; t < ptr[j + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(a[pp[t]], u[row[t]]));
-  out[j] = acc;
+  out[j] = gather_dot(ptr[j], ptr[j + 1], a, [&](int64_t t) { return pp[t]; }, u,
+                      [&](int64_t t) { return row[t]; });
 }
 
 // D = (Sigma_s + dw) C, C = 1 / (dc Sigma_s + (1 + dc dw)) per row
@@ -170,8 +186,8 @@ __global__ void rhs_cols_kernel(int64_t n, const int64_t *ptr, const int32_t *pp
   if (j >= n) return;
   const double q_x = __dsub_rn(__dadd_rn(pv.x[j], __dmul_rn(inv_or_zero(st.dxl[j]), pv.zxl[j])),
                                __dmul_rn(inv_or_zero(st.dxu[j]), pv.zxu[j]));
-  double acc = 0.0;
-  for (int64_t t = ptr[j]; t < ptr[j + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(st.a[pp[t]], u[row[t]]));
+  const double acc = gather_dot(ptr[j], ptr[j + 1], st.a, [&](int64_t t) { return pp[t]; }, u,
+                                [&](int64_t t) { return row[t]; });
   qx[j] = q_x;
   rhs[j] = __dadd_rn(q_x, acc);
 }
@@ -181,8 +197,8 @@ __global__ void recover_sd_kernel(int64_t m, const int64_t *rowptr, const int32_
                                   double *dy) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= m) return;
-  double ax = 0.0;
-  for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) ax = __dadd_rn(ax, __dmul_rn(st.a[p], dx[col[p]]));
+  const double ax = gather_dot(rowptr[i], rowptr[i + 1], st.a, [](int64_t p) { return p; }, dx,
+                               [&](int64_t p) { return col[p]; });
   const double c = c_of(st, st.ss[i]);
   const double dsi = __dmul_rn(c, __dsub_rn(__dadd_rn(ax, __dmul_rn(st.dc, qs[i])), qy[i]));
   ds[i] = dsi;
@@ -208,10 +224,10 @@ __global__ void residual_x_kernel(int64_t n, const int64_t *wptr, const int32_t 
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; j < n;
        j += static_cast<int64_t>(gridDim.x) * kT) {
     const double dxj = step.x[j];
-    dd wv = {0.0, 0.0};
-    for (int64_t t = wptr[j]; t < wptr[j + 1]; ++t) wv = dd_add(wv, dd_prod(st.w[wp[t]], step.x[wj[t]]));
-    dd atv = {0.0, 0.0};
-    for (int64_t t = atptr[j]; t < atptr[j + 1]; ++t) atv = dd_add(atv, dd_prod(st.a[atp[t]], step.y[atrow[t]]));
+    const dd wv = dd_gather_dot(wptr[j], wptr[j + 1], st.w, [&](int64_t t) { return wp[t]; }, step.x,
+                                [&](int64_t t) { return wj[t]; });
+    const dd atv = dd_gather_dot(atptr[j], atptr[j + 1], st.a, [&](int64_t t) { return atp[t]; }, step.y,
+                                 [&](int64_t t) { return atrow[t]; });
     dd rx = dd_from(pv.x[j]);
     rx = dd_add(rx, dd_neg(wv));
     rx = dd_add(rx, dd_neg(dd_prod(st.dw, dxj)));
@@ -241,8 +257,8 @@ __global__ void residual_s_kernel(int64_t m, const int64_t *rowptr, const int32_
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * kT) {
     const double dsi = step.s[i], dyi = step.y[i];
-    dd ax = {0.0, 0.0};
-    for (int64_t p = rowptr[i]; p < rowptr[i + 1]; ++p) ax = dd_add(ax, dd_prod(st.a[p], step.x[col[p]]));
+    const dd ax = dd_gather_dot(rowptr[i], rowptr[i + 1], st.a, [](int64_t p) { return p; }, step.x,
+                                [&](int64_t p) { return col[p]; });
     dd r_s = dd_add(dd_from(pv.s[i]), dd_neg(dd_prod(st.dw, dsi)));
     r_s = dd_add(r_s, dd_from(dyi));
     r_s = dd_add(r_s, dd_from(step.zsl[i]));
