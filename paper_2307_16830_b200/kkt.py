@@ -205,8 +205,10 @@ class HostAnalysis:
         import os
         import time
 
-        # leave one core to the launching thread (device setup runs there)
-        L.lib().gn_set_host_threads(max(1, len(os.sched_getaffinity(0)) - 1))
+        # this process's share of the host cores (one process per GPU under
+        # torchrun), minus one for the launching thread (device setup)
+        share = len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+        L.lib().gn_set_host_threads(max(1, share - 1))
         try:
             t = time.perf_counter()
             self._cs = symbolic_condense(model.hess_rows, model.hess_cols, model.jac_rows,
