@@ -480,7 +480,7 @@ def main():
     # DRAM traffic of one refactorisation from the committed ncu capture of
     # the same kernels (profiles/, tools/profile_round.sh), C3 only
     traffic = None
-    tpath = os.path.join(HERE, "profiles", "r01c_traffic_C3.json")
+    tpath = os.path.join(HERE, "profiles", "r01e_traffic_C3.json")
     if args.workload == "C3" and os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get("refactor_bytes_per_launch")
@@ -512,7 +512,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "refactorisation (mf_factor_small + mf_factor_large + mf_factor_top)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "traffic_source": "profiles/r01c_traffic_C3.json (ncu, cold L2)",
+                     "traffic": traffic, "traffic_source": "profiles/r01e_traffic_C3.json (ncu, cold L2)",
                      "alg_bytes_per_launch": alg_bytes,
                      "mean_launch_ms": ref["mean_ms"]},
         "rooflines_secondary": secondary,
