@@ -14,6 +14,7 @@
 #include <memory>
 #include <cmath>
 
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <queue>
@@ -721,6 +722,9 @@ static void front_plan(Symbolic &S) {
   // top fronts: the highest complete levels of the large part holding at
   // most kTopFronts fronts, all of them tall (the cluster kernel's share)
   S.nf_top = 0;
+  const char *e_tf = std::getenv("GN_TOP_FRONTS"), *e_tr = std::getenv("GN_TOP_MIN_ROWS");
+  const int64_t top_fronts = e_tf ? std::atoll(e_tf) : kTopFronts;
+  const int64_t top_min_rows = e_tr ? std::atoll(e_tr) : kTopMinRows;
   {
     int64_t k = nf, lev = -1;
     while (k > S.nf_small) {
@@ -728,8 +732,8 @@ static void front_plan(Symbolic &S) {
       int64_t b = k;
       while (b > S.nf_small && S.level[S.order[b - 1]] == l) --b;
       bool tall = true;
-      for (int64_t q = b; q < k; ++q) tall = tall && S.f_nrows[S.order[q]] >= kTopMinRows;
-      if (!tall || nf - b > kTopFronts) break;
+      for (int64_t q = b; q < k; ++q) tall = tall && S.f_nrows[S.order[q]] >= top_min_rows;
+      if (!tall || nf - b > top_fronts) break;
       k = b;
       lev = l;
     }
