@@ -180,6 +180,19 @@ class _Timer:
         return {k: sum(a.elapsed_time(b) for a, b in v) / 1e3 for k, v in self.spans.items()}
 
 
+def _resident(model, name, host):
+    """Device copy of a host array that is constant for the model (bounds,
+    start point, ranges): kept on the model with its host value and reused
+    while the value is unchanged (dropped by ``release_device``)."""
+    cache = model.__dict__.setdefault("_resident_inputs", {})
+    hit = cache.get(name)
+    if hit is not None and hit[0].shape == host.shape and np.array_equal(hit[0], host):
+        return hit[1]
+    dev = D.to_dev(host)
+    cache[name] = (host.copy(), dev)
+    return dev
+
+
 class _DeviceSolve:
     """Device buffers and scalar mailboxes of one solve."""
 
@@ -203,7 +216,7 @@ class _DeviceSolve:
         # frozen gradient scaling at x0 (ipm.py:179-193), on the device: the
         # scale factors, the relaxed slack bounds and the initial slacks are
         # torch ops; one scalar read later brings obj_scale and theta0 back
-        x0d = D.to_dev(self.x0)
+        x0d = _resident(model, "x0", self.x0)
         g0 = D.empty(n)
         j0 = D.empty(max(1, model.nnz_jac))
         self.ev.flags.zero_()
@@ -231,7 +244,7 @@ class _DeviceSolve:
         # relax_equalities (ipm.py:112-123) on the scaled ranges
         if m:
             tol = self.tol_r
-            rlo_d, rhi_d = D.to_dev(self.rlo), D.to_dev(self.rhi)
+            rlo_d, rhi_d = _resident(model, "rlo", self.rlo), _resident(model, "rhi", self.rhi)
             lo, hi = rlo_d * self.con_scale, rhi_d * self.con_scale
             one = torch.ones_like(lo)
             inf = torch.full_like(lo, np.inf)
@@ -242,7 +255,7 @@ class _DeviceSolve:
         # scaling keeps finiteness, so the bound count needs no device data
         self.n_bounds = int(np.isfinite(xl).sum() + np.isfinite(xu).sum()
                             + np.isfinite(self.rlo).sum() + np.isfinite(self.rhi).sum())
-        self.xl, self.xu = D.to_dev(xl), D.to_dev(xu)
+        self.xl, self.xu = _resident(model, "xl", xl), _resident(model, "xu", xu)
         self.x = x0d.clone()
         self.s, self.y = D.zeros(m), D.zeros(m)
         fin = lambda t: torch.isfinite(t).to(torch.float64)
