@@ -180,17 +180,39 @@ class _Timer:
         return {k: sum(a.elapsed_time(b) for a, b in v) / 1e3 for k, v in self.spans.items()}
 
 
-def _resident(model, name, host):
-    """Device copy of a host array that is constant for the model (bounds,
-    start point, ranges): kept on the model with its host value and reused
-    while the value is unchanged (dropped by ``release_device``)."""
-    cache = model.__dict__.setdefault("_resident_inputs", {})
-    hit = cache.get(name)
-    if hit is not None and hit[0].shape == host.shape and np.array_equal(hit[0], host):
-        return hit[1]
-    dev = D.to_dev(host)
-    cache[name] = (host.copy(), dev)
-    return dev
+def _prepared_inputs(model, opts, ranges) -> dict:
+    """Bounds with fixed variables widened, the pushed-in start point, the
+    constraint ranges and the bound count (host and device), prepared once
+    and kept on the model while the raw inputs are unchanged (compared by
+    value; dropped by ``release_device``)."""
+    m = model.n_con
+    rr = None if ranges is None else np.asarray(ranges, dtype=float)
+    raw = (model.lower, model.upper, model.start, rr)
+    c = model.__dict__.get("_prepared_inputs")
+    if c is not None and c["eps"] == opts.fixed_var_eps and all(
+            (a is None and b is None) or (a is not None and b is not None and a.shape == b.shape
+                                          and np.array_equal(a, b))
+            for a, b in zip(c["raw"], raw)):
+        return c
+    xl, xu = model.lower.copy(), model.upper.copy()
+    fixed = xl == xu
+    if np.any(fixed):
+        eps = opts.fixed_var_eps * np.maximum(1.0, np.abs(xl))
+        xl, xu = np.where(fixed, xl - eps, xl), np.where(fixed, xu + eps, xu)
+    x0 = np.minimum(np.maximum(model.start, xl), xu)
+    if rr is None:
+        rlo, rhi = np.zeros(m), np.zeros(m)
+    else:
+        rlo, rhi = rr[:, 0].copy(), rr[:, 1].copy()
+    c = {"eps": opts.fixed_var_eps, "raw": tuple(None if a is None else a.copy() for a in raw),
+         "xl": xl, "xu": xu, "x0": x0, "rlo": rlo, "rhi": rhi,
+         # scaling keeps finiteness, so the bound count needs no device data
+         "n_bounds": int(np.isfinite(xl).sum() + np.isfinite(xu).sum()
+                         + np.isfinite(rlo).sum() + np.isfinite(rhi).sum()),
+         "xl_d": D.to_dev(xl), "xu_d": D.to_dev(xu), "x0_d": D.to_dev(x0),
+         "rlo_d": D.to_dev(rlo) if m else None, "rhi_d": D.to_dev(rhi) if m else None}
+    model.__dict__["_prepared_inputs"] = c
+    return c
 
 
 class _DeviceSolve:
@@ -202,13 +224,10 @@ class _DeviceSolve:
         n, m = model.n_var, model.n_con
         self.n, self.m = n, m
         self.tol_r = opts.bound_relax if opts.bound_relax is not None else opts.tol
-        xl, xu = model.lower.copy(), model.upper.copy()
-        fixed = xl == xu
-        if np.any(fixed):
-            eps = opts.fixed_var_eps * np.maximum(1.0, np.abs(xl))
-            xl, xu = np.where(fixed, xl - eps, xl), np.where(fixed, xu + eps, xu)
+        pin = _prepared_inputs(model, opts, ranges)
+        xl, xu = pin["xl"], pin["xu"]
         self.xl_h, self.xu_h = xl, xu
-        self.x0 = np.minimum(np.maximum(model.start, xl), xu)
+        self.x0 = pin["x0"]
         self.ev = evaluator(model)
         dev = D.require_cuda()
         self.dev = dev
@@ -216,17 +235,14 @@ class _DeviceSolve:
         # frozen gradient scaling at x0 (ipm.py:179-193), on the device: the
         # scale factors, the relaxed slack bounds and the initial slacks are
         # torch ops; one scalar read later brings obj_scale and theta0 back
-        x0d = _resident(model, "x0", self.x0)
+        x0d = pin["x0_d"]
         g0 = D.empty(n)
         j0 = D.empty(max(1, model.nnz_jac))
         self.ev.flags.zero_()
         self.ev.launch(x0d, GRAD | JAC, grad=g0, jac=j0)
         self.flags0 = self.ev.flags.clone()
-        if ranges is None:
-            self.rlo, self.rhi = np.zeros(m), np.zeros(m)
-        else:
-            r = np.asarray(ranges, dtype=float)
-            self.rlo, self.rhi = r[:, 0].copy(), r[:, 1].copy()
+        self.rlo, self.rhi = pin["rlo"], pin["rhi"]
+        self.rlo_d, self.rhi_d = pin["rlo_d"], pin["rhi_d"]
         if opts.scaling:
             gm = g0.abs().max() if n else torch.zeros((), dtype=torch.float64, device=dev)
             self.obj_scale_d = torch.where(gm > 0, torch.clamp(100.0 / gm, max=1.0), torch.ones_like(gm))
@@ -244,7 +260,7 @@ class _DeviceSolve:
         # relax_equalities (ipm.py:112-123) on the scaled ranges
         if m:
             tol = self.tol_r
-            rlo_d, rhi_d = _resident(model, "rlo", self.rlo), _resident(model, "rhi", self.rhi)
+            rlo_d, rhi_d = pin["rlo_d"], pin["rhi_d"]
             lo, hi = rlo_d * self.con_scale, rhi_d * self.con_scale
             one = torch.ones_like(lo)
             inf = torch.full_like(lo, np.inf)
@@ -252,10 +268,8 @@ class _DeviceSolve:
             self.su = torch.where(torch.isfinite(hi), hi + tol * torch.maximum(one, hi.abs()), inf)
         else:
             self.sl, self.su = D.zeros(1), D.zeros(1)
-        # scaling keeps finiteness, so the bound count needs no device data
-        self.n_bounds = int(np.isfinite(xl).sum() + np.isfinite(xu).sum()
-                            + np.isfinite(self.rlo).sum() + np.isfinite(self.rhi).sum())
-        self.xl, self.xu = _resident(model, "xl", xl), _resident(model, "xu", xu)
+        self.n_bounds = pin["n_bounds"]
+        self.xl, self.xu = pin["xl_d"], pin["xu_d"]
         self.x = x0d.clone()
         self.s, self.y = D.zeros(m), D.zeros(m)
         fin = lambda t: torch.isfinite(t).to(torch.float64)
@@ -367,8 +381,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             if m:
                 g = P.ct[:m]
                 zero = torch.zeros_like(g)
-                viol = torch.maximum(torch.maximum(D.to_dev(P.rlo) - g, zero),
-                                     torch.maximum(g - D.to_dev(P.rhi), zero))
+                viol = torch.maximum(torch.maximum(P.rlo_d - g, zero),
+                                     torch.maximum(g - P.rhi_d, zero))
                 P.scal[63] = viol.max()
             P.flags[0:1].copy_(ev.flags)
             fin, adf, _ = P.read(62, 64)
