@@ -450,23 +450,30 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     ev_flags = ev.flags
 
     pv_buf = PVec.empty(n, m)
-    for _ in range(opts.max_iter):
-        mu = state["mu"]
-        # ---- derivatives at x (ipm.py:384-391)
+
+    def launch_eval_prep(mu):
+        """Derivatives at x (ipm.py:384-391), then widths, Sigma, residual
+        blocks and reductions (ipm.py:393-429) and the async read of their
+        scalars.  Issued right after the previous iteration's accept, ahead
+        of its host bookkeeping."""
         t0 = timer.start()
         with span("ad_full"):
             ev.launch(P.x, F | C | GRAD | JAC | HESS | RESET, y=P.y, obj_weight=P.obj_scale,
                       con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
                       grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
         timer.stop("ad", t0)
-        # ---- widths, Sigma, residual blocks and reductions (ipm.py:393-429)
         cands = _mu_candidates(mu, mu_min, opts, L.IPM_MAX_MU)
         mus = (ctypes.c_double * len(cands))(*cands)
         with span("prep"):
             L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal),
                                     stream))
         P.flags[0:1].copy_(ev_flags)
-        ev_prep = P.read_async(0, 49)
+        return P.read_async(0, 49), cands
+
+    pending = launch_eval_prep(state["mu"]) if opts.max_iter > 0 else None
+    for _ in range(opts.max_iter):
+        mu = state["mu"]
+        ev_prep, cands = pending
         # the condensed matrix does not depend on mu: assemble and factor it
         # (delta_w = delta_c = 0, the first try of kkt.py:424-447) while the
         # host reads the residuals and runs the barrier update; the PD flag is
@@ -610,6 +617,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         L.check(lib.gn_ipm_accept(ws.handle, ctypes.byref(V), ctypes.byref(stc), alpha, alpha_z,
                                   mu, opts.kappa_sigma, L.ptr(P.flags[1:2]), stream))
         state["it"] += 1
+        if state["it"] < opts.max_iter:   # the next iteration's device work first
+            pending = launch_eval_prep(state["mu"])
         if opts.record_trace:
             report.trace.append((state["it"], fval / P.obj_scale, float(primal_max),
                                  float(dual_max), mu, alpha, delta_w))
