@@ -24,6 +24,30 @@
 
 namespace gn {
 
+// Per-thread key histograms -> bucket pointers and per-(thread, key) start
+// offsets (stable: thread chunks in order inside a key).  The totals and the
+// offsets are parallel over keys; only the prefix over keys is serial.
+static void merge_histograms(std::vector<std::vector<int64_t>> &hist, int64_t nkeys, int nt,
+                             std::vector<int64_t> &ptr) {
+  ptr.assign(nkeys + 1, 0);
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t c = 0; c < nkeys; ++c) {
+    int64_t tot = 0;
+    for (int t = 0; t < nt; ++t) tot += hist[t][c];
+    ptr[c + 1] = tot;
+  }
+  for (int64_t c = 0; c < nkeys; ++c) ptr[c + 1] += ptr[c];
+#pragma omp parallel for num_threads(nt) schedule(static)
+  for (int64_t c = 0; c < nkeys; ++c) {
+    int64_t run = ptr[c];
+    for (int t = 0; t < nt; ++t) {
+      const int64_t h = hist[t][c];
+      hist[t][c] = run;
+      run += h;
+    }
+  }
+}
+
 // (row, col) coordinates -> lower CSC with sorted unique rows per column, and
 // the slot of every input coordinate (the np.unique(col<<32|row) inverse of
 // csc.py:52-76).  Bucketed by column: O(nnz + sum_c u_c log u_c).
@@ -43,16 +67,8 @@ static void csc_from_coords(int64_t n, const std::vector<int32_t> &rows, const s
     auto [lo, hi] = chunk(t);
     for (int64_t q = lo; q < hi; ++q) hist[t][cols[q]]++;
   }
-  std::vector<int64_t> bptr(n + 1, 0);
-  for (int64_t c = 0; c < n; ++c) {
-    int64_t run = bptr[c];
-    for (int t = 0; t < nt; ++t) {
-      const int64_t h = hist[t][c];
-      hist[t][c] = run;
-      run += h;
-    }
-    bptr[c + 1] = run;
-  }
+  std::vector<int64_t> bptr;
+  merge_histograms(hist, n, nt, bptr);
   std::vector<int32_t> bucket(K);
 #pragma omp parallel for num_threads(nt) schedule(static, 1)
   for (int t = 0; t < nt; ++t) {
@@ -115,16 +131,7 @@ static void par_bucket(int64_t nkeys, int64_t N, KeyFn key, PlaceFn place, std::
     auto [lo, hi] = chunk(t);
     for (int64_t i = lo; i < hi; ++i) hist[t][key(i)]++;
   }
-  ptr.assign(nkeys + 1, 0);
-  for (int64_t c = 0; c < nkeys; ++c) {
-    int64_t run = ptr[c];
-    for (int t = 0; t < nt; ++t) {
-      const int64_t h = hist[t][c];
-      hist[t][c] = run;
-      run += h;
-    }
-    ptr[c + 1] = run;
-  }
+  merge_histograms(hist, nkeys, nt, ptr);
 #pragma omp parallel for num_threads(nt) schedule(static, 1)
   for (int t = 0; t < nt; ++t) {
     auto [lo, hi] = chunk(t);
