@@ -104,21 +104,69 @@ def build_model(workload, seed=None):
     return build_acopf(parse_matpower(tiled_case(WORKLOADS[workload], seed=seed)))
 
 
-def cpu_baseline(workload, tol, am=None):
-    """Oracle port of the reference on one host core, ordering injected."""
-    from oracle import ipm as OI
-    from oracle import model as OM
-    from paper_2307_16830_b200 import kkt, sparse
+def workload_config(workload, tol, n_var, n_con, world=1):
+    """The `config` object, identical in both arms (the driver compares them)."""
+    return {"workload": f"{workload}: {WORKLOADS[workload]} IEEE-14 tiles on a "
+                        f"{_cols(WORKLOADS[workload])}-column mesh with angle/thermal limits, "
+                        f"tol {tol:g}",
+            "n_var": int(n_var), "n_con": int(n_con),
+            "l2": "flushed between steps (512 MiB write, outside the timed events)",
+            "parallelism": "replicas" if world > 1 else "single instance"}
 
-    am = am or build_model(workload)
-    m = am.model
-    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
-    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
-    perm = sparse.amd_order(cs.matrix)   # bit-identical to amd_order; injected (loop-fair)
+
+def _cols(tiles):
+    import math
+
+    return math.ceil(math.sqrt(tiles))
+
+
+def host_info(cores_used):
+    """CPU model and core counts of this host."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "affinity_cores": len(os.sched_getaffinity(0)),
+            "cores_used": cores_used}
+
+
+def oracle_instance(tiles, seed=None):
+    """The reference path's inputs built by the oracle alone (no product
+    library): model (oracle/acopf.py restating src/acopf.py) and the
+    reference ordering (heap minimum degree, bit-identical to amd_order);
+    C4 uses the committed permutation of the golden run."""
+    from oracle import acopf as OA
+    from paper_2307_16830_b200.grids import tiled_case
+    from paper_2307_16830_b200.matpower import parse_matpower
+
+    oa = OA.build(parse_matpower(tiled_case(tiles, seed=seed)))
+    gp = os.path.join(HERE, "tests", "golden", "C4_perm.npz")
+    if tiles == WORKLOADS["C4"] and seed is None and os.path.exists(gp):
+        perm = np.load(gp)["perm"].astype(np.int64)
+    else:
+        perm = OA.ordering(oa)
+    return oa, perm
+
+
+def oracle_solve(oa, perm, tol):
+    """One loop-fair solve by the oracle port (ordering injected)."""
+    from oracle import ipm as OI
+
     t = time.perf_counter()
-    rep = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol), am.ranges, ordering=perm)
-    dt = time.perf_counter() - t
-    return dt, rep
+    rep = OI.solve(oa.model, oa.lower, oa.upper, oa.start, OI.Options(tol=tol), oa.ranges,
+                   ordering=perm)
+    return time.perf_counter() - t, rep
+
+
+def cpu_baseline(workload, tol, inst=None):
+    """Oracle port of the reference on one host core, ordering injected."""
+    oa, perm = inst or oracle_instance(WORKLOADS[workload])
+    return oracle_solve(oa, perm, tol)
 
 
 def run_reference(args):
@@ -126,22 +174,15 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import psutil  # noqa: F401  (available in the image)
-
-    am = build_model(args.workload)
-    warm = build_model("C1")
-    from oracle import ipm as OI
-    from oracle import model as OM
-
-    wm = warm.model
-    wom = OM.expand(wm.n_var, wm.n_con, OM.from_model(wm))
+    oa, perm = oracle_instance(WORKLOADS[args.workload])
+    warm, wperm = oracle_instance(1)
     for _ in range(args.warmup):   # warm the code paths on the 14-bus tile
-        OI.solve(wom, wm.lower, wm.upper, wm.start, OI.Options(tol=args.tol), warm.ranges)
+        oracle_solve(warm, wperm, args.tol)
     times, rep = [], None
     budget = float(os.environ.get("REF_BUDGET_S", "240"))
     t_all = time.perf_counter()
     for k in range(args.steps):
-        dt, rep = cpu_baseline(args.workload, args.tol, am)
+        dt, rep = oracle_solve(oa, perm, args.tol)
         times.append(dt)
         if time.perf_counter() - t_all > budget and k + 1 < args.steps:
             break
@@ -152,12 +193,13 @@ def run_reference(args):
         "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * v, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {WORKLOADS[args.workload]} IEEE-14 tiles, limits, "
-                               f"tol {args.tol:g}", "n_var": am.model.n_var, "n_con": am.model.n_con},
+        "config": workload_config(args.workload, args.tol, oa.model.n, oa.model.m, args.gpus),
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
                          "sample": f"full {args.workload} solve to tol {args.tol:g} "
                                    f"({rep.iterations} IPM iterations) per step, ordering injected "
-                                   "(loop-fair); warm-up on the 14-bus tile"},
+                                   "(loop-fair); model and ordering built by oracle/ alone; "
+                                   "warm-up on the 14-bus tile",
+                         **host_info(cores)},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iterations": rep.iterations, "objective": rep.objective, "status": rep.status,
     }
@@ -172,21 +214,7 @@ def _c5_worker(seed):
 
 
 def cpu_baseline_instance(tiles, seed, tol):
-    from oracle import ipm as OI
-    from oracle import model as OM
-    from paper_2307_16830_b200 import kkt, sparse
-    from paper_2307_16830_b200.acopf import build_acopf
-    from paper_2307_16830_b200.grids import tiled_case
-    from paper_2307_16830_b200.matpower import parse_matpower
-
-    am = build_acopf(parse_matpower(tiled_case(tiles, seed=seed)))
-    m = am.model
-    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
-    cs = kkt.symbolic_condense(m.hess_rows, m.hess_cols, m.jac_rows, m.jac_cols, m.n_var)
-    perm = sparse.amd_order(cs.matrix)
-    t = time.perf_counter()
-    rep = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol), am.ranges, ordering=perm)
-    return time.perf_counter() - t, rep
+    return oracle_solve(*oracle_instance(tiles, seed), tol)
 
 
 def run_batch_reference(args):
@@ -213,15 +241,25 @@ def run_batch_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": 1, "ms_per_step": 1e3 * v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C5: batch of {args.batch} load-perturbed 1,358-bus instances, tol 1e-6"},
+        "config": batch_config(args, args.gpus),
         "cpu_baseline": {"value": v, "unit": "s", "cores": cores, "kind": "port",
                          "sample": f"{sample} instances solved in parallel on {cores} processes per step, "
-                                   f"projected to {args.batch} (ordering injected, loop-fair)"},
+                                   f"projected to {args.batch} (ordering injected, loop-fair; model "
+                                   "and ordering built by oracle/ alone)",
+                         **host_info(cores)},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "instances_per_s": args.batch / v,
         "statuses": sorted({r[1] for r in res}),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def batch_config(args, world):
+    return {"workload": f"C5: batch of {args.batch} load-perturbed 1,358-bus instances "
+                        f"(12142 vars / 17515 cons each), tol {args.tol:g}",
+            "parallelism": f"instances partitioned over {world} GPU(s) / host processes, "
+                           "one final gather"}
 
 
 def run_batch(args):
@@ -284,10 +322,8 @@ def run_batch(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * v, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md Appendix B, loads x (1+U(-0.1,0.1)), seed = instance index)",
-        "config": {"workload": f"C5: batch of {args.batch} load-perturbed 1,358-bus instances "
-                               f"({n_var} vars each), tol {args.tol:g}",
-                   "parallelism": f"instances partitioned over {world} GPU(s), {args.concurrency} "
-                                  "concurrent solves per GPU, one final gather"},
+        "config": batch_config(args, world),
+        "concurrency": f"{args.concurrency} concurrent solves per GPU",
         "instances_per_s": args.batch / v,
         "optimal": int(sum(s == "optimal" for s in stat)), "mean_iterations": float(np.mean(its)),
         "e2e": None, "clocks": clk, "gpu_launches": launches,
@@ -488,11 +524,13 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            dt, orep = cpu_baseline(args.workload, args.tol, am)
+            dt, orep = cpu_baseline(args.workload, args.tol)
             cpu = {"value": dt, "unit": "s", "cores": 1, "kind": "port",
                    "sample": f"one full {args.workload} solve to tol {args.tol:g} "
                              f"({orep.iterations} iterations, objective {orep.objective:.10g}) by the "
-                             "oracle port, ordering injected (loop-fair)"}
+                             "oracle port, ordering injected (loop-fair); model and ordering built "
+                             "by oracle/ alone",
+                   **host_info(1)}
         except Exception as exc:  # never fail the bench line on the baseline leg
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
@@ -501,12 +539,9 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md Appendix B IEEE-14 tiling, no load perturbation)",
-        "config": {"workload": f"{args.workload}: {model.n_var} vars / {model.n_con} cons "
-                               f"({WORKLOADS[args.workload]} IEEE-14 tiles, limits), tol {args.tol:g}",
-                   "nnz_jac": model.nnz_jac, "nnz_hess": model.nnz_hess, "nnz_K": nnz_k,
-                   "nnz_L": nnz_l, "fronts": info["n_fronts"], "front_levels": info["n_levels"],
-                   "l2": "flushed between steps (512 MiB write, outside the timed events)",
-                   "parallelism": "replicas" if world > 1 else "single instance"},
+        "config": workload_config(args.workload, args.tol, model.n_var, model.n_con, world),
+        "structure": {"nnz_jac": model.nnz_jac, "nnz_hess": model.nnz_hess, "nnz_K": nnz_k,
+                      "nnz_L": nnz_l, "fronts": info["n_fronts"], "front_levels": info["n_levels"]},
         "iterations": iters, "objective": rep.objective, "status": rep.status,
         "per_iter_ms": per_iter,
         "roofline": {"bound": "hbm", "kernel": "refactorisation (mf_factor_small + mf_factor_large + mf_factor_top)",

@@ -187,6 +187,10 @@ int gn_chol_solve(gn_symbolic *sym, const double *fronts, const double *b, doubl
  * persistent kernels (which need every CTA co-resident) are sized to 1/k of
  * the device from now on (thread-local; default 1). */
 int gn_set_concurrency(int k);
+/* Return every cached device block of the plan allocator to the driver
+ * (freed plan memory is otherwise kept for reuse, invisible to torch's
+ * allocator).  cached_bytes_before (may be NULL) receives the cache size. */
+int gn_alloc_trim(int64_t *cached_bytes_before);
 /* Diagnostics: when trace (device int64[3][n_fronts][4]) is non-NULL the
  * factor / forward / backward kernels stamp %globaltimer per front (task
  * start, dependencies met, assembled, done).  NULL turns it off. */

@@ -3,25 +3,35 @@
 // Plans are created per solve and dropped with the model, so a process that
 // solves case after case would otherwise pay cudaMalloc's page mapping
 // (~0.3 ms per array on B200) on every solve.  Freed blocks are kept in a
-// per-device cache keyed by rounded size and handed out again; a block goes
-// back to the cache only after the device has finished with it (the same
-// device-wide synchronisation cudaFree performs), so reuse needs no stream
-// bookkeeping.  GN_ALLOC_CACHE=0 disables the cache.
+// per-device cache keyed by rounded size and handed out again.
+//
+// A freed block may still be in use by work queued on any stream, so it is
+// first parked on a per-device PENDING list; freeing never synchronises.  An
+// allocation that finds no ready block of its size but a pending one waits
+// for the device once (one cudaDeviceSynchronize for the whole pending list,
+// instead of one per free) and then reuses it.  Concurrent solves on other
+// threads are therefore only stalled by an allocation that actually reuses
+// memory, never by a teardown.  `gn_alloc_trim` returns every cached block
+// to the driver (torch's allocator cannot see this cache; device.py calls it
+// on a torch out-of-memory error and from `release_all`).  GN_ALLOC_CACHE=0
+// disables the cache.
 #include <cstdlib>
 #include <map>
 #include <mutex>
 #include <unordered_map>
+#include <vector>
 
 #include "device.cuh"
 
 namespace gn {
 namespace {
 
-constexpr size_t kCacheLimit = size_t(8) << 30;   // bytes kept per device
+constexpr size_t kCacheLimit = size_t(8) << 30;   // bytes kept per device (ready + pending)
 
 struct Cache {
   std::mutex mu;
-  std::multimap<size_t, void *> free_blocks[64];   // per device: rounded size -> block
+  std::multimap<size_t, void *> ready[64];     // per device: rounded size -> block, device done with it
+  std::multimap<size_t, void *> pending[64];   // freed, possibly still referenced by queued work
   size_t cached[64] = {};
   std::unordered_map<void *, std::pair<int, size_t>> live;   // block -> (device, rounded size)
 };
@@ -47,6 +57,17 @@ size_t round_size(size_t b) {
   return (b + q - 1) / q * q;
 }
 
+// caller holds c.mu; `dev` is the current device
+void *take(Cache &c, int dev, size_t r) {
+  auto it = c.ready[dev].find(r);
+  if (it == c.ready[dev].end()) return nullptr;
+  void *p = it->second;
+  c.ready[dev].erase(it);
+  c.cached[dev] -= r;
+  c.live[p] = {dev, r};
+  return p;
+}
+
 }  // namespace
 
 void *dev_malloc(size_t bytes) {
@@ -61,15 +82,22 @@ void *dev_malloc(size_t bytes) {
     GN_REQUIRE(dev >= 0 && dev < 64, "device ordinal out of range");
     const size_t r = round_size(bytes);
     Cache &c = cache();
+    bool drain = false;
     {
       std::lock_guard<std::mutex> g(c.mu);
-      auto it = c.free_blocks[dev].find(r);
-      if (it != c.free_blocks[dev].end()) {
-        p = it->second;
-        c.free_blocks[dev].erase(it);
-        c.cached[dev] -= r;
-        c.live[p] = {dev, r};
-      }
+      p = take(c, dev, r);
+      drain = !p && c.pending[dev].count(r) > 0;
+    }
+    if (drain) {
+      // a pending block of this size exists: wait for the device once, then
+      // every pending block of the device is ready
+      GN_CUDA(cudaDeviceSynchronize());
+      std::lock_guard<std::mutex> g(c.mu);
+      // only blocks parked before the synchronisation are moved (a block
+      // freed meanwhile by another thread stays pending)
+      for (auto &kv : c.pending[dev]) c.ready[dev].emplace(kv.first, kv.second);
+      c.pending[dev].clear();
+      p = take(c, dev, r);
     }
     if (!p) {
       GN_CUDA(cudaMalloc(&p, r));
@@ -88,32 +116,57 @@ void dev_free(void *p) {
     return;
   }
   Cache &c = cache();
-  int dev;
-  size_t r;
+  bool keep = false;
   {
     std::lock_guard<std::mutex> g(c.mu);
     auto it = c.live.find(p);
     if (it == c.live.end()) return;
-    dev = it->second.first;
-    r = it->second.second;
+    const int dev = it->second.first;
+    const size_t r = it->second.second;
     c.live.erase(it);
-  }
-  // the device must be done with the block before anyone may reuse it
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (cur != dev) cudaSetDevice(dev);
-  const bool ok = cudaDeviceSynchronize() == cudaSuccess;
-  bool keep = false;
-  if (ok) {
-    std::lock_guard<std::mutex> g(c.mu);
     if (c.cached[dev] + r <= kCacheLimit) {
-      c.free_blocks[dev].emplace(r, p);
+      c.pending[dev].emplace(r, p);
       c.cached[dev] += r;
       keep = true;
     }
   }
-  if (!keep) cudaFree(p);
-  if (cur != dev) cudaSetDevice(cur);
+  if (!keep) cudaFree(p);   // cudaFree itself waits for the device
+}
+
+void alloc_trim() {
+  if (!cache_on()) return;
+  Cache &c = cache();
+  std::vector<std::pair<int, void *>> out;
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    for (int d = 0; d < 64; ++d) {
+      for (auto &kv : c.ready[d]) out.emplace_back(d, kv.second);
+      for (auto &kv : c.pending[d]) out.emplace_back(d, kv.second);
+      c.ready[d].clear();
+      c.pending[d].clear();
+      c.cached[d] = 0;
+    }
+  }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto &dp : out) {
+    if (dp.first != cur) cudaSetDevice(dp.first);
+    cudaFree(dp.second);
+    if (dp.first != cur) cudaSetDevice(cur);
+  }
 }
 
 }  // namespace gn
+
+extern "C" int gn_alloc_trim(int64_t *cached_bytes_before) {
+  return gn::guarded([&] {
+    if (cached_bytes_before) {
+      gn::Cache &c = gn::cache();
+      std::lock_guard<std::mutex> g(c.mu);
+      int64_t s = 0;
+      for (int d = 0; d < 64; ++d) s += static_cast<int64_t>(c.cached[d]);
+      *cached_bytes_before = s;
+    }
+    gn::alloc_trim();
+  });
+}

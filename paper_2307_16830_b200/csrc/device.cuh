@@ -35,6 +35,7 @@ void add_upload_time(double malloc_s, double copy_s);
 
 void *dev_malloc(size_t bytes);   // cached device allocation (alloc.cu)
 void dev_free(void *p);
+void alloc_trim();               // return cached blocks to the driver
 
 template <class T>
 T *dev_upload(const std::vector<T> &v) {

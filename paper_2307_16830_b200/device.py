@@ -52,12 +52,34 @@ def to_dev(a, dtype=torch.float64):
     return t
 
 
+def trim_plan_cache() -> int:
+    """Return the native plan allocator's cached blocks to the driver
+    (gn_alloc_trim) and torch's cached blocks too; returns the native cache
+    size before trimming (bytes)."""
+    import ctypes
+
+    from . import _lib as L
+
+    before = ctypes.c_int64()
+    L.check(L.lib().gn_alloc_trim(ctypes.byref(before)))
+    torch.cuda.empty_cache()
+    return before.value
+
+
+def _retry_oom(fn):
+    try:
+        return fn()
+    except torch.OutOfMemoryError:   # the plan cache may hold the memory torch needs
+        trim_plan_cache()
+        return fn()
+
+
 def empty(n, dtype=torch.float64):
-    return torch.empty(int(n), dtype=dtype, device=require_cuda())
+    return _retry_oom(lambda: torch.empty(int(n), dtype=dtype, device=require_cuda()))
 
 
 def zeros(n, dtype=torch.float64):
-    return torch.zeros(int(n), dtype=dtype, device=require_cuda())
+    return _retry_oom(lambda: torch.zeros(int(n), dtype=dtype, device=require_cuda()))
 
 
 def is_tensor(a) -> bool:

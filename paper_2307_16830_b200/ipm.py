@@ -321,9 +321,14 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     # symbolic analysis (condensed pattern, ordering, symbolic factor, device
     # plans) is a function of the sparsity only: cached on the model.  On a
     # miss its host part starts on a worker thread right away.
-    key = None if opts.ordering is None else id(opts.ordering)
+    # keyed on the ordering's CONTENT (a copy is kept): a new array that
+    # reuses a freed one's id, or one mutated in place, is a different key
+    key = None if opts.ordering is None else np.array(opts.ordering, dtype=np.int64, copy=True)
     cache = getattr(model, "_kkt_cache", None)
-    analysis = HostAnalysis(model, opts.ordering) if cache is None or cache[0] != key else None
+    hit = cache is not None and ((cache[0] is None and key is None) or (
+        cache[0] is not None and key is not None and cache[0].shape == key.shape
+        and np.array_equal(cache[0], key)))
+    analysis = None if hit else HostAnalysis(model, opts.ordering)
     try:
         P = _DeviceSolve(model, opts, constraint_ranges)
         setup["problem"] = time.perf_counter() - t_start
@@ -386,11 +391,16 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
                 P.scal[63] = viol.max()
             P.flags[0:1].copy_(ev.flags)
             fin, adf, _ = P.read(62, 64)
-            ev.raise_on_flags(adf)
-            report.objective = float(fin[0])
-            report.constraint_violation = float(fin[1]) if m else 0.0
+            # ipm.py:352-355: a non-finite objective leaves both NaN; a
+            # non-finite g(x) keeps the objective and leaves the violation NaN
+            if not adf & F:
+                report.objective = float(fin[0])
+                if not adf & C:
+                    report.constraint_violation = float(fin[1]) if m else 0.0
         except NonFiniteResult:
             pass
+        if state.get("reg") is not None:   # the last Newton step's regularisation
+            ws.delta_w, ws.delta_c = state["reg"]
         sec = timer.totals()
         internal = max(0.0, total - sec["ad"] - sec["linear"])
         report.seconds = {"total": total, "ad": sec["ad"], "linear": sec["linear"],
@@ -434,10 +444,16 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     P.flags[1:2].copy_(P.flags0)
     sc0, adf0, adf_x0 = P.read(60, 62)
     if adf_x0:
+        # the scaling evaluations at x0 failed: _Problem's constructor raised
+        # in the reference (ipm.py:305-312), so the report carries no x
         try:
             ev.raise_on_flags(adf_x0, order=(GRAD, JAC))
         except NonFiniteResult as exc:
-            return finish(EVAL_ERROR, str(exc))
+            report.status = EVAL_ERROR
+            report.message = str(exc)
+            report.seconds = {"total": time.perf_counter() - t_start, "ad": 0.0, "linear": 0.0,
+                              "internal": 0.0}
+            return report
     P.flags.zero_()
     if adf0:
         return finish(EVAL_ERROR, "constraint evaluation produced a non-finite value")
@@ -547,6 +563,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             timer.stop("linear", t0)
             return finish(REGULARIZATION_EXHAUSTED, str(exc))
         timer.stop("linear", t0)
+        state["reg"] = (ws.delta_w, ws.delta_c)
         report.refinement_relative_residual = ir.relative_residual
         # ---- fraction to the boundary and dphi (ipm.py:455-476)
         tau = max(opts.tau_min, 1.0 - mu)
