@@ -27,7 +27,8 @@ def pytest_collection_modifyitems(config, items):
             it.add_marker(skip)
 
 
-MODEL_TAGS = ("case14", "case118", "C1", "T4")
+MODEL_TAGS = ("case14", "case118", "C1", "T4", "C2")
+TILES = {"C1": 1, "T4": 4, "C2": 143}
 
 
 @pytest.fixture(scope="session")

@@ -85,3 +85,35 @@ def test_invariants_determinism_mu_alpha_filter():
             assert theta < th or phi < ph
     sec = r1.seconds
     assert sec["ad"] + sec["linear"] + sec["internal"] <= sec["total"] * 1.001
+
+
+def nonconvex_model():
+    """Concave objective (negative curvature at the start) with one equality:
+    the speculative delta_w = 0 factorisation is not positive definite, so
+    the inertia correction of kkt.py:424-447 runs inside the solve."""
+    b = box(3, -1.0, 2.0, 0.0)
+    b.add_objective(-(var(0) - param(0)) ** 2 + 0.5 * var(0) * var(1),
+                    np.array([[0, 1], [1, 2], [2, 0]]), np.array([[0.3], [0.1], [-0.2]]))
+    b.add_constraints(var(0) + var(1) + var(2) - 1.0, np.array([[0, 1, 2]]), np.zeros((1, 0)))
+    return b.finalize()
+
+
+@pytest.mark.parametrize("tol", (1e-4, 1e-8))
+def test_regularization_inside_solve_matches_oracle(tol):
+    """delta_w schedule inside the IPM (ipm.py:441-447): every iteration's
+    delta_w, the iteration count and the solution equal the oracle's (which
+    restates the reference loop with the dense-free condensed backend)."""
+    from oracle import ipm as OI
+    from oracle import model as OM
+
+    m = nonconvex_model()
+    rep = solve(m, SolverOptions(tol=tol))
+    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
+    orep = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol))
+    assert rep.status == orep.status
+    assert rep.iterations == orep.iterations
+    dws = [row[6] for row in rep.trace]
+    assert any(dw > 0 for dw in dws), "the correction path was not exercised"
+    assert dws == [row[6] for row in orep.trace]
+    assert rep.objective == pytest.approx(orep.objective, rel=1e-9, abs=1e-12)
+    np.testing.assert_allclose(rep.x, orep.x, atol=1e-7)

@@ -14,7 +14,7 @@ from oracle import kkt as OK
 from oracle import model as OM
 from oracle import sparse as OS
 
-from conftest import MODEL_TAGS, golden_x
+from conftest import MODEL_TAGS, TILES, golden_x
 from golden_io import oracle_model
 
 pytestmark = pytest.mark.gpu
@@ -43,7 +43,7 @@ def normwise(a, b, tol):
 def product_model(tag, networks_json):
     if tag.startswith("case"):
         return build_acopf(network_from_tables(networks_json[tag]))
-    return build_acopf(parse_matpower(tiled_case({"C1": 1, "T4": 4}[tag])))
+    return build_acopf(parse_matpower(tiled_case(TILES[tag])))
 
 
 # ---------------------------------------------------------------- AD (a4-a10)
@@ -337,7 +337,7 @@ def test_end_to_end_ieee_cases(networks_json, end_to_end, case, tol):
 
 
 @pytest.mark.parametrize("tag,tiles,seed", [("C1", 1, None), ("T16", 16, None), ("C5s0", 97, 0),
-                                            ("C2", 143, None)])
+                                            ("C5s1", 97, 1), ("C5s2", 97, 2), ("C2", 143, None)])
 def test_end_to_end_synthetic(end_to_end, tag, tiles, seed):
     am = build_acopf(parse_matpower(tiled_case(tiles, seed=seed)))
     rep = gp.solve(am.model, gp.SolverOptions(tol=1e-6), constraint_ranges=am.ranges)
@@ -367,7 +367,7 @@ def test_generated_pattern_kernels_match_interpreter():
     import os
 
     for tag in ("C1", "T4"):
-        tiles = {"C1": 1, "T4": 4}[tag]
+        tiles = TILES[tag]
         outs = {}
         for mode in ("interp", "patterns"):
             if mode == "interp":

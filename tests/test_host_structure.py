@@ -18,13 +18,13 @@ from paper_2307_16830_b200.matpower import network_from_tables, parse_matpower
 from paper_2307_16830_b200.model import ModelBuilder
 from paper_2307_16830_b200.expressions import param, sin, var
 
-from conftest import MODEL_TAGS
+from conftest import MODEL_TAGS, TILES
 
 
 def product_model(tag, networks_json):
     if tag.startswith("case"):
         return build_acopf(network_from_tables(networks_json[tag]))
-    tiles = {"C1": 1, "T4": 4}[tag]
+    tiles = TILES[tag]
     return build_acopf(parse_matpower(tiled_case(tiles)))
 
 
