@@ -285,10 +285,16 @@ def run_batch(args):
     opts = SolverOptions(tol=args.tol)
     clocks = _clock_sampler() if rank == 0 else None
     time.sleep(1.0)
-    solve_fn = (lambda xs: BT.solve_batch_concurrent(xs, opts, args.concurrency)) if args.concurrency > 1 \
-        else (lambda xs: BT.solve_batch(xs, opts))
+    if args.c5_mode == "batched":      # K12: one launch per kernel for the rank's whole block
+        from paper_2307_16830_b200.batch_ipm import solve_batched
+
+        solve_fn = lambda xs: solve_batched(xs, opts)
+    elif args.c5_mode == "concurrent":
+        solve_fn = lambda xs: BT.solve_batch_concurrent(xs, opts, args.concurrency)
+    else:
+        solve_fn = lambda xs: BT.solve_batch(xs, opts)
     for _ in range(max(1, args.warmup)):
-        solve_fn(inst[:2 * max(1, args.concurrency)])
+        solve_fn(inst)
     _lib.stats(reset=True)
     times = []
     full = None
@@ -323,7 +329,9 @@ def run_batch(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md Appendix B, loads x (1+U(-0.1,0.1)), seed = instance index)",
         "config": batch_config(args, world),
-        "concurrency": f"{args.concurrency} concurrent solves per GPU",
+        "mode": {"batched": "instance-batched kernels (one launch per kernel for the rank's block)",
+                 "concurrent": f"{args.concurrency} concurrent single solves per GPU",
+                 "sequential": "single solves back to back"}[args.c5_mode],
         "instances_per_s": args.batch / v,
         "optimal": int(sum(s == "optimal" for s in stat)), "mean_iterations": float(np.mean(its)),
         "e2e": None, "clocks": clk, "gpu_launches": launches,
@@ -344,7 +352,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--batch", type=int, default=256, help="C5: number of instances")
     ap.add_argument("--concurrency", type=int, default=2,
-                    help="C5: concurrent solves per GPU (host threads x CUDA streams)")
+                    help="C5 concurrent mode: solves per GPU (host threads x CUDA streams)")
+    ap.add_argument("--c5-mode", default="batched", choices=("batched", "concurrent", "sequential"))
     args = ap.parse_args()
     if args.workload == "C5":
         return run_batch_reference(args) if args.impl == "reference" else run_batch(args)

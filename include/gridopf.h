@@ -274,6 +274,25 @@ typedef struct gn_ipm_vecs {
   double *dual_x, *dual_s, *primal;            /* KKT residual blocks            */
 } gn_ipm_vecs;
 
+/* ------------------------------------------------------------------ */
+/* Instance batches: B problems of ONE sparsity pattern share
+ * every plan (model, KKT, symbolic factor); their vectors are stored
+ * instance-major ([B][n], [B][m], [B][nnzH], [B][nnzJ], [B][nnzK], fronts
+ * [B][front_doubles], solve workspace [B][vec_doubles]) and each *_batched
+ * entry point is one launch per kernel for all B instances.  Per-instance
+ * scalar operands are read from a device array bp[B][GN_BP_STRIDE]; scalar
+ * outputs go to per-instance blocks scal + b * GN_BATCH_SCAL. */
+#define GN_BP_MU 0         /* barrier parameter                                */
+#define GN_BP_TAU 1        /* fraction-to-boundary factor                      */
+#define GN_BP_ALPHA 2      /* primal step (trial point, accept, axpy)          */
+#define GN_BP_ALPHA_Z 3    /* dual step (accept)                               */
+#define GN_BP_DW 4         /* delta_w                                          */
+#define GN_BP_DC 5         /* delta_c                                          */
+#define GN_BP_ACTIVE 6     /* 0: state-changing kernels leave the instance alone */
+#define GN_BP_OBJW 7       /* objective weight / scale (AD)                    */
+#define GN_BP_STRIDE 8
+#define GN_BATCH_SCAL 64   /* doubles per instance in batched scalar blocks    */
+
 /* layout of the scalar block written by gn_ipm_prep (device doubles) */
 #define GN_IPM_MAX_MU 16
 #define GN_PREP_X_DUAL 0     /* max |dual_x|                         */
@@ -319,6 +338,64 @@ int gn_ipm_trial_merit(gn_kkt *k, const gn_ipm_vecs *v, const double *ct, const 
  * interiority (ipm.py:521-548) */
 int gn_ipm_accept(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                   double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream);
+
+
+/* ---- batched entry points (K12; layout and bp/scal conventions above).
+ * Each replaces B back-to-back calls of its single-instance counterpart on
+ * B problems sharing one plan -- the reference's multi-instance path is
+ * run_suite(parallel=P) over independent solves (src/bench.py:166-186). */
+/* gn_ad_eval for B instances: x [B][n], y/con_scale [B][m], c [B][m], grad
+ * [B][n], jac [B][nnzJ], hess [B][nnzH]; objw_b / objs_b [B] objective
+ * weight (Hessian) and scale (f, gradient), NULL = 1; params_b [B][P] per-
+ * instance parameter values in the plan's layout (gn_model_param_count),
+ * NULL = the model's own; f at f + b f_stride; flags [B]; contrib_ws [B][..] */
+int gn_ad_eval_batched(gn_model *mdl, int32_t B, const double *x, const double *y, const double *objw_b,
+                       const double *con_scale, const double *objs_b, const double *params_b, double *f,
+                       int64_t f_stride, double *c, double *grad, double *jac, double *hess, uint32_t what,
+                       double *contrib_ws, int32_t *flags, void *stream);
+/* size P of the device parameter layout (per pattern block: param slot-major) */
+int gn_model_param_count(const gn_model *mdl, int64_t *count);
+/* kvals [B][nnzK]; delta_w / delta_c from bp */
+int gn_kkt_assemble_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *bp, double *kvals,
+                            void *stream);
+int gn_kkt_condense_rhs_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *bp, const gn_vec7 *pv,
+                                double *qx, double *qs, double *qy, double *rhs, void *stream);
+int gn_kkt_recover_slack_dual_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *bp,
+                                      const double *dx, const double *qs, const double *qy, double *ds, double *dy,
+                                      void *stream);
+/* flags [B] */
+int gn_kkt_recover_bound_duals_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *dx,
+                                       const double *ds, const gn_vec7 *pv, double *dzxl, double *dzxu,
+                                       double *dzsl, double *dzsu, int32_t *flags, void *stream);
+/* norm: instance b's residual max at norm[b * GN_BATCH_SCAL] (+1 scratch) */
+int gn_kkt_residual_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *bp, const gn_vec7 *steps,
+                            const gn_vec7 *pv, gn_vec7 *res, double *norm, void *stream);
+int gn_kkt_matrix_scale_batched(gn_kkt *k, int32_t B, const gn_kkt_state *st, const double *bp, double *out,
+                                void *stream);
+/* y += bp[b].alpha * x per instance (alpha 0: instance untouched) */
+int gn_vec7_axpy_batched(gn_kkt *k, int32_t B, gn_vec7 *y, const gn_vec7 *x, const double *bp, void *stream);
+/* fronts [B][front_doubles], fail_pos [B] (instance-local positions) */
+int gn_chol_factor_batched(gn_symbolic *sym, int32_t B, const double *kvals, double *fronts, int64_t *fail_pos,
+                           void *stream);
+/* b, x [B][n], ws [B][vec_doubles] */
+int gn_chol_solve_batched(gn_symbolic *sym, int32_t B, const double *fronts, const double *b, double *x,
+                          double *ws, void *stream);
+/* mus_dev [B][GN_IPM_MAX_MU] barrier candidates; scal [B][GN_BATCH_SCAL] */
+int gn_ipm_prep_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, int32_t n_mu, const double *mus_dev,
+                        double *scal, void *stream);
+int gn_ipm_pvec_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const double *bp, gn_vec7 *pv, void *stream);
+int gn_ipm_direction_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps, const double *bp,
+                             double *scal, void *stream);
+int gn_ipm_trial_point_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps, const double *bp,
+                               double *xt, double *st, void *stream);
+/* alpha = min of the pair at alpha_pairs + b * GN_BATCH_SCAL */
+int gn_ipm_trial_point_at_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                  const double *alpha_pairs, double *xt, double *st, void *stream);
+int gn_ipm_trial_merit_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const double *ct, const double *xt,
+                               const double *st, double *scal, void *stream);
+/* instances with bp[b].active == 0 are left untouched; flags [B] */
+int gn_ipm_accept_batched(gn_kkt *k, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps, const double *bp,
+                          double kappa_sigma, int32_t *flags, void *stream);
 
 #ifdef __cplusplus
 }

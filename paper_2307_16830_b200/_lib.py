@@ -110,6 +110,25 @@ _SIGS = {
     "gn_ipm_trial_merit": (c_i32, [P, P, P, P, P, P, P]),
     "gn_ipm_trial_point_at": (c_i32, [P, P, P, P, P, P, P]),
     "gn_ipm_accept": (c_i32, [P, P, P, c_dbl, c_dbl, c_dbl, c_dbl, P, P]),
+    # batched (K12)
+    "gn_ad_eval_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P, c_i64, P, P, P, P, c_u32, P, P, P]),
+    "gn_model_param_count": (c_i32, [P, P]),
+    "gn_kkt_assemble_batched": (c_i32, [P, c_i32, P, P, P, P]),
+    "gn_kkt_condense_rhs_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P, P]),
+    "gn_kkt_recover_slack_dual_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P, P]),
+    "gn_kkt_recover_bound_duals_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P, P, P, P]),
+    "gn_kkt_residual_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P]),
+    "gn_kkt_matrix_scale_batched": (c_i32, [P, c_i32, P, P, P, P]),
+    "gn_vec7_axpy_batched": (c_i32, [P, c_i32, P, P, P, P]),
+    "gn_chol_factor_batched": (c_i32, [P, c_i32, P, P, P, P]),
+    "gn_chol_solve_batched": (c_i32, [P, c_i32, P, P, P, P, P]),
+    "gn_ipm_prep_batched": (c_i32, [P, c_i32, P, c_i32, P, P, P]),
+    "gn_ipm_pvec_batched": (c_i32, [P, c_i32, P, P, P, P]),
+    "gn_ipm_direction_batched": (c_i32, [P, c_i32, P, P, P, P, P]),
+    "gn_ipm_trial_point_batched": (c_i32, [P, c_i32, P, P, P, P, P, P]),
+    "gn_ipm_trial_point_at_batched": (c_i32, [P, c_i32, P, P, P, P, P, P]),
+    "gn_ipm_trial_merit_batched": (c_i32, [P, c_i32, P, P, P, P, P, P]),
+    "gn_ipm_accept_batched": (c_i32, [P, c_i32, P, P, P, c_dbl, P, P]),
 }
 
 _lib = None

@@ -280,6 +280,10 @@ struct GatherArgs {
   GatherSeg seg[4];
   int nseg;
   int64_t begin[5];
+  // instance batches (blockIdx.y): contributions per instance, scale vectors
+  // (con_scale) per instance, scalar (obj_scale) from scal_b[instance]
+  int64_t contrib_stride, scale_stride;
+  const double *scal_b;
 };
 
 __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contrib, int32_t *flags) {
@@ -289,6 +293,9 @@ __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contr
   while (t >= ga.begin[s + 1]) ++s;
   const GatherSeg &G = ga.seg[s];
   int64_t o = t - ga.begin[s];
+  const int64_t bi = blockIdx.y;
+  contrib += bi * ga.contrib_stride;
+  flags += bi;
   double acc = 0.0;
   const int64_t p1 = G.ptr[o + 1];
   for (int64_t p = G.ptr[o]; p < p1; p += 4) {   // four terms' loads in flight, same order
@@ -304,17 +311,19 @@ __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contr
   }
   if (!isfinite(acc)) atomicOr(flags, G.bit);
   double sc = 1.0;
-  if (G.mode == 1) sc = G.scalar;
-  else if (G.mode == 2 && G.scale) sc = G.scale[o];
-  else if (G.mode == 3 && G.scale) sc = G.scale[G.rows[o]];
-  G.out[o] = G.mode == 0 ? acc : acc * sc;
+  const double *scale = G.scale ? G.scale + bi * ga.scale_stride : nullptr;
+  if (G.mode == 1) sc = ga.scal_b ? ga.scal_b[bi] : G.scalar;
+  else if (G.mode == 2 && scale) sc = scale[o];
+  else if (G.mode == 3 && scale) sc = scale[G.rows[o]];
+  G.out[bi * G.n_out + o] = G.mode == 0 ? acc : acc * sc;
 }
 
 // non-finite check of directly written outputs (the gather does it otherwise)
 __global__ void finite_check_kernel(int64_t n, const double *__restrict__ v, int32_t *flags, int32_t bit) {
   int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  v += static_cast<int64_t>(blockIdx.y) * n;   // instance batches: [B][n] values, [B] flags
   bool bad = t < n && !isfinite(v[t]);
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, bit);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags + blockIdx.y, bit);
 }
 
 // Objective: the flattened contribution list (block order) in contiguous
@@ -324,9 +333,18 @@ constexpr int kObjThreads = 256;
 constexpr int kObjMaxCtas = 128;
 __global__ void __launch_bounds__(kObjThreads)
 ad_objective_kernel(const int32_t *__restrict__ src, int64_t total, const double *__restrict__ contrib,
-                    double scale, double *f, int32_t *flags, double *partials, unsigned *counter) {
+                    double scale, double *f, int32_t *flags, double *partials, unsigned *counter,
+                    int64_t contrib_stride, int64_t f_stride, const double *scale_b) {
   __shared__ double red[kObjThreads];
   __shared__ bool last;
+  // instance batches (blockIdx.y): own contributions, partials, counter, output
+  const int64_t bi = blockIdx.y;
+  contrib += bi * contrib_stride;
+  partials += bi * kObjMaxCtas;
+  counter += bi;
+  flags += bi;
+  f += bi * f_stride;
+  if (scale_b) scale = scale_b[bi];
   const int64_t per = (total + gridDim.x - 1) / gridDim.x;
   const int64_t lo = per * blockIdx.x, hi = min(total, lo + per);
   double part = 0.0;
@@ -368,6 +386,10 @@ static void release_model(Model &M) {
   if (!M.uploaded) return;
   dev_free(M.d.jslots);
   M.d.jslots = nullptr;
+  dev_free(M.d.bstrides);
+  dev_free(M.d.bstrides_shared);
+  M.d.bstrides = M.d.bstrides_shared = nullptr;
+  M.batch_cap = 0;
   dev_free(M.d.obj_partials);
   dev_free(M.d.obj_counter);
   M.d.obj_partials = nullptr;
@@ -457,6 +479,8 @@ static void upload_model(Model &M) {
   M.d.obj_block_ptr = dev_upload(M.obj_block_ptr);
   M.d.obj_partials = dev_alloc<double>(kObjMaxCtas);
   M.d.obj_counter = dev_upload(std::vector<unsigned>{0u});
+  M.batch_cap = 1;
+  M.n_params = static_cast<int64_t>(par.size());
   M.d.n_obj_blocks = static_cast<int32_t>(M.obj_block_ptr.size()) - 1;
   M.d.jac_rows = dev_upload(narrow<int32_t>(M.jac_rows));
   // pattern kernels generated from the tapes (NVRTC, cached per source)
@@ -492,14 +516,39 @@ static void upload_model(Model &M) {
   M.uploaded = true;
 }
 
+// Batched (B > 1, K12): every instance has its own x / y / con_scale /
+// parameters / outputs (instance-major, strides n, m, nnz, params) and its
+// own objective weight and scale (device arrays objw_b / objs_b, [B]); the
+// plan -- record indices, tapes, gather lists -- is shared.  f has stride
+// f_stride, flags one word per instance.
 static void ad_eval(Model &M, const double *x, const double *y, double obj_w, const double *con_scale,
                     double obj_scale, double *f, double *c, double *grad, double *jac, double *hess,
-                    uint32_t what, double *contrib, int32_t *flags, cudaStream_t st) {
+                    uint32_t what, double *contrib, int32_t *flags, cudaStream_t st, int B = 1,
+                    const double *params_b = nullptr, const double *objw_b = nullptr,
+                    const double *objs_b = nullptr, int64_t f_stride = 0) {
   GN_REQUIRE(M.uploaded, "model not uploaded to the device");
+  GN_REQUIRE(B >= 1, "batch size must be positive");
   if (what & GN_AD_HESS) GN_REQUIRE(y != nullptr || M.m == 0, "Hessian needs multipliers");
+  if (B > 1) GN_REQUIRE(M.pattern_fn != nullptr, "batched AD needs the generated pattern kernels (NVRTC)");
   if (what & GN_AD_RESET_FLAGS) {
-    GN_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t), st));
+    GN_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * B, st));
     what &= ~GN_AD_RESET_FLAGS;
+  }
+  if (B > M.batch_cap) {   // objective reduction scratch for B instances
+    GN_CUDA(cudaStreamSynchronize(st));
+    dev_free(M.d.obj_partials);
+    dev_free(M.d.obj_counter);
+    M.d.obj_partials = dev_alloc<double>(static_cast<int64_t>(kObjMaxCtas) * B);
+    M.d.obj_counter = dev_alloc<unsigned>(B);
+    GN_CUDA(cudaMemset(M.d.obj_counter, 0, sizeof(unsigned) * B));
+    M.batch_cap = B;
+  }
+  const int64_t par_size = static_cast<int64_t>(M.n_params);
+  if (B > 1 && !M.d.bstrides) {
+    const std::vector<long long> bs = {static_cast<long long>(M.n), static_cast<long long>(M.m),
+                                       static_cast<long long>(M.n_contrib), static_cast<long long>(par_size),
+                                       static_cast<long long>(M.jac_rows.size())};
+    M.d.bstrides = dev_upload(bs);
   }
   if (M.n_ctas_rec > 0 && M.pattern_fn) {
     int nblk = static_cast<int>(M.dblocks.size());
@@ -510,8 +559,23 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
     const int32_t *jsl = M.d.jslots;
     int jdirect = (M.jac_direct && (what & GN_AD_JAC)) ? 1 : 0;
     double *jac_out = jac;
-    void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib, &jsl, &jac_out, &jdirect};
-    GN_REQUIRE(launch_patterns(M.pattern_fn, static_cast<unsigned>(M.n_ctas_rec), st, args),
+    if (B > 1 && params_b) pa = params_b;   // per-instance parameter values, shared layout
+    const long long *bs = B > 1 ? M.d.bstrides : nullptr;
+    // shared parameters: stride 0 (bs[3] is the per-instance layout size)
+    const long long *bs_use = bs;
+    if (B > 1 && !params_b) {
+      if (!M.d.bstrides_shared) {
+        const std::vector<long long> b2 = {static_cast<long long>(M.n), static_cast<long long>(M.m),
+                                           static_cast<long long>(M.n_contrib), 0LL,
+                                           static_cast<long long>(M.jac_rows.size())};
+        M.d.bstrides_shared = dev_upload(b2);
+      }
+      bs_use = M.d.bstrides_shared;
+    }
+    void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib, &jsl, &jac_out, &jdirect,
+                    &bs_use, &objw_b};
+    GN_REQUIRE(launch_patterns(M.pattern_fn, static_cast<unsigned>(M.n_ctas_rec), st, args,
+                               static_cast<unsigned>(B)),
                "pattern kernel launch failed");
     count_launch();
   } else if (M.n_ctas_rec > 0) {
@@ -531,31 +595,39 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
     ++ns;
   };
   ga.begin[0] = 0;
+  ga.contrib_stride = M.n_contrib;
+  ga.scale_stride = M.m;
+  ga.scal_b = objs_b;
   if (what & GN_AD_C) add(M.m, M.d.c_ptr, M.d.c_src, c, con_scale ? 2 : 0, 1.0, con_scale, nullptr, GN_AD_C);
-  if (what & GN_AD_GRAD) add(M.n, M.d.grad_ptr, M.d.grad_src, grad, obj_scale != 1.0 ? 1 : 0, obj_scale, nullptr, nullptr, GN_AD_GRAD);
+  if (what & GN_AD_GRAD)
+    add(M.n, M.d.grad_ptr, M.d.grad_src, grad, (obj_scale != 1.0 || objs_b) ? 1 : 0, obj_scale, nullptr, nullptr,
+        GN_AD_GRAD);
   if ((what & GN_AD_JAC) && !(M.pattern_fn && M.jac_direct))
     add(static_cast<int64_t>(M.jac_rows.size()), M.d.jac_ptr, M.d.jac_src, jac, con_scale ? 3 : 0, 1.0,
         con_scale, M.d.jac_rows, GN_AD_JAC);
   if ((what & GN_AD_JAC) && M.pattern_fn && M.jac_direct && !M.jac_rows.empty()) {
     const int64_t nj = static_cast<int64_t>(M.jac_rows.size());
-    GN_LAUNCH(finite_check_kernel, static_cast<unsigned>((nj + 255) / 256), 256, 0, st, nj, jac, flags, GN_AD_JAC);
+    GN_LAUNCH(finite_check_kernel, dim3(static_cast<unsigned>((nj + 255) / 256), B), 256, 0, st, nj, jac, flags,
+              GN_AD_JAC);
   }
   if (what & GN_AD_HESS)
     add(static_cast<int64_t>(M.hess_rows.size()), M.d.hess_ptr, M.d.hess_src, hess, 0, 1.0, nullptr, nullptr, GN_AD_HESS);
   ga.nseg = ns;
   if (ns > 0) {
     int64_t tot = ga.begin[ns];
-    GN_LAUNCH(ad_gather_kernel, static_cast<unsigned>((tot + 255) / 256), 256, 0, st, ga, contrib, flags);
+    GN_LAUNCH(ad_gather_kernel, dim3(static_cast<unsigned>((tot + 255) / 256), B), 256, 0, st, ga, contrib, flags);
     GN_LAUNCH_CHECK();
   }
   if (what & GN_AD_F) {
     const int64_t total = static_cast<int64_t>(M.obj_src.size());
     if (total > 0) {
       const int g = static_cast<int>(std::min<int64_t>(kObjMaxCtas, (total + 4095) / 4096));
-      GN_LAUNCH(ad_objective_kernel, g, kObjThreads, 0, st, M.d.obj_src, total, contrib, obj_scale, f, flags,
-                M.d.obj_partials, M.d.obj_counter);
-    } else {
+      GN_LAUNCH(ad_objective_kernel, dim3(g, B), kObjThreads, 0, st, M.d.obj_src, total, contrib, obj_scale, f,
+                flags, M.d.obj_partials, M.d.obj_counter, M.n_contrib, f_stride, objs_b);
+    } else if (B == 1) {
       GN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), st));
+    } else {
+      GN_CUDA(cudaMemset2DAsync(f, sizeof(double) * f_stride, 0, sizeof(double), B, st));
     }
   }
 }
@@ -563,6 +635,20 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
 }  // namespace gn
 
 using namespace gn;
+
+extern "C" int gn_ad_eval_batched(gn_model *M, int32_t B, const double *x, const double *y, const double *objw_b,
+                                  const double *con_scale, const double *objs_b, const double *params_b, double *f,
+                                  int64_t f_stride, double *c, double *grad, double *jac, double *hess,
+                                  uint32_t what, double *contrib_ws, int32_t *flags, void *stream) {
+  return guarded([&] {
+    ad_eval(*M, x, y, 1.0, con_scale, 1.0, f, c, grad, jac, hess, what, contrib_ws, flags,
+            static_cast<cudaStream_t>(stream), B, params_b, objw_b, objs_b, f_stride);
+  });
+}
+
+extern "C" int gn_model_param_count(const gn_model *M, int64_t *count) {
+  return guarded([&] { *count = static_cast<int64_t>(M->n_params); });
+}
 
 extern "C" int gn_model_upload(gn_model *M) {
   return guarded([&] {

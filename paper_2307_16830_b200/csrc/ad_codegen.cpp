@@ -389,7 +389,19 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
     << ") gn_ad_patterns(const GenBlk *__restrict__ blks, int nblk, const int *__restrict__ var_idx, "
        "const double *__restrict__ params, const int *__restrict__ targets, const double *__restrict__ x, "
        "const double *__restrict__ y, const double *__restrict__ cs, double obj_w, unsigned what, "
-       "double *__restrict__ contrib, const int *__restrict__ jslots, double *__restrict__ jac, int jdirect) {\n"
+       "double *__restrict__ contrib, const int *__restrict__ jslots, double *__restrict__ jac, int jdirect,\n"
+       "    const long long *__restrict__ bs, const double *__restrict__ objw_b) {\n"
+       "  // instance batches: blockIdx.y = instance, bs = strides (x, y and con_scale, contrib, params, jac)\n"
+       "  if (bs) {\n"
+       "    const long long bi = blockIdx.y;\n"
+       "    x += bi * bs[0];\n"
+       "    if (y) y += bi * bs[1];\n"
+       "    if (cs) cs += bi * bs[1];\n"
+       "    contrib += bi * bs[2];\n"
+       "    params += bi * bs[3];\n"
+       "    if (jac) jac += bi * bs[4];\n"
+       "    if (objw_b) obj_w = objw_b[bi];\n"
+       "  }\n"
        "  int lo = 0, hi = nblk - 1;\n"
        "  while (lo < hi) {\n"
        "    const int mid = (lo + hi + 1) >> 1;\n"
@@ -452,8 +464,8 @@ void *compile_patterns(const std::string &src, std::string &err) {
   return fn;
 }
 
-bool launch_patterns(void *fn, unsigned grid, void *stream, void **args) {
-  return api().launch(fn, grid, 1, 1, kPatternThreads, 1, 1, 0, stream, args, nullptr) == 0;
+bool launch_patterns(void *fn, unsigned grid, void *stream, void **args, unsigned batch) {
+  return api().launch(fn, grid, batch, 1, kPatternThreads, 1, 1, 0, stream, args, nullptr) == 0;
 }
 
 }  // namespace gn

@@ -16,6 +16,6 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of);
 // compiled kernel (a CUfunction), cached process-wide by source; nullptr
 // with `err` set when NVRTC or the driver API is unavailable
 void *compile_patterns(const std::string &src, std::string &err);
-bool launch_patterns(void *fn, unsigned grid, void *stream, void **args);
+bool launch_patterns(void *fn, unsigned grid, void *stream, void **args, unsigned batch = 1);
 
 }  // namespace gn

@@ -114,6 +114,8 @@ struct Model {
   void *d_genblk = nullptr;          // its per-block table (device)
   std::string pattern_error;         // why the interpreter is used, if it is
   bool jac_direct = false;           // every J slot has exactly one contribution
+  int batch_cap = 0;                 // instances the objective scratch holds
+  int64_t n_params = 0;              // device parameter layout size (doubles)
   struct Dev {
     DevBlock *blocks = nullptr;
     int32_t *tape = nullptr;  // int4-packed (op, a, b, 0)
@@ -131,6 +133,8 @@ struct Model {
     int32_t *jslots = nullptr;       // Jacobian slot per constraint contribution (direct writes)
     double *obj_partials = nullptr;  // objective reduction scratch
     unsigned *obj_counter = nullptr;
+    long long *bstrides = nullptr;   // batched strides (x, y/cs, contrib, params, jac)
+    long long *bstrides_shared = nullptr;   // same with shared parameters
   } d;
   ~Model();
 };
@@ -209,6 +213,7 @@ struct Symbolic {
   int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
   int64_t flops = 0;
   long long *trace = nullptr;   // optional device [3][nf][4] timing stamps
+  int64_t counters_cap = 0;     // instances the dependency-counter array holds
   // device
   bool uploaded = false;
   struct Dev {
@@ -234,6 +239,7 @@ struct Symbolic {
 struct Kkt {
   int64_t n = 0, m = 0, nh = 0, nj = 0, nk = 0, np = 0;
   bool has_assembly = false;
+  int batch_cap = 0;     // instances the reduction / m-vector scratch holds
   struct Dev {
     int64_t *a_rowptr = nullptr;   // A by rows (jac order)
     int32_t *a_col = nullptr;

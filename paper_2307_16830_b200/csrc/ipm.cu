@@ -21,21 +21,28 @@ __device__ __forceinline__ double width_hi(double v, double b) { return isfinite
 struct MuList {
   int n;
   double mu[GN_IPM_MAX_MU];
+  const double *dev;   // batched: [B][GN_IPM_MAX_MU] candidates on the device
 };
 
-RedSpec spec(Kkt &K, double *out, int k, const int *ops) {
+__device__ __forceinline__ double mu_k(const MuList &mus, int k) {
+  return mus.dev ? mus.dev[blockIdx.y * GN_IPM_MAX_MU + k] : mus.mu[k];
+}
+
+RedSpec spec(Kkt &K, double *out, int k, const int *ops, int64_t out_stride = 0) {
   RedSpec r{};
   r.k = k;
   for (int i = 0; i < k; ++i) r.op[i] = ops[i];
   r.out = out;
   r.partials = K.d.partials;
   r.counter = K.d.counter;
+  r.out_stride = out_stride;
   return r;
 }
 
 __global__ void __launch_bounds__(kRedThreads)
 prep_x_kernel(int64_t n, const int64_t *atptr, const int32_t *atp, const int32_t *atrow, gn_ipm_vecs v,
-              MuList mus, RedSpec rs) {
+              MuList mus, RedSpec rs, Bx bx) {
+  shift(v, bx);
   double acc[4 + GN_IPM_MAX_MU];
   acc[0] = 0.0;
   acc[1] = 0.0;
@@ -61,8 +68,9 @@ prep_x_kernel(int64_t n, const int64_t *atptr, const int32_t *atp, const int32_t
     if (fu) acc[3] += log(wu);
     for (int k = 0; k < mus.n; ++k) {
       double c = 0.0;
-      if (fl) c = fabs(zl * wl - mus.mu[k]);
-      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mus.mu[k]));
+      const double mk = mu_k(mus, k);
+      if (fl) c = fabs(zl * wl - mk);
+      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mk));
       acc[4 + k] = red_combine(RED_MAX, acc[4 + k], c);
     }
   }
@@ -70,7 +78,8 @@ prep_x_kernel(int64_t n, const int64_t *atptr, const int32_t *atp, const int32_t
 }
 
 __global__ void __launch_bounds__(kRedThreads)
-prep_s_kernel(int64_t m, gn_ipm_vecs v, MuList mus, RedSpec rs) {
+prep_s_kernel(int64_t m, gn_ipm_vecs v, MuList mus, RedSpec rs, Bx bx) {
+  shift(v, bx);
   double acc[7 + GN_IPM_MAX_MU];
   for (int k = 0; k < 7 + mus.n; ++k) acc[k] = 0.0;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < m;
@@ -95,15 +104,19 @@ prep_s_kernel(int64_t m, gn_ipm_vecs v, MuList mus, RedSpec rs) {
     if (fu) acc[6] += log(wu);
     for (int k = 0; k < mus.n; ++k) {
       double c = 0.0;
-      if (fl) c = fabs(zl * wl - mus.mu[k]);
-      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mus.mu[k]));
+      const double mk = mu_k(mus, k);
+      if (fl) c = fabs(zl * wl - mk);
+      if (fu) c = red_combine(RED_MAX, c, fabs(zu * wu - mk));
       acc[7 + k] = red_combine(RED_MAX, acc[7 + k], c);
     }
   }
   grid_reduce(rs, acc);
 }
 
-__global__ void pvec_kernel(int64_t n, int64_t m, gn_ipm_vecs v, double mu, gn_vec7 pv) {
+__global__ void pvec_kernel(int64_t n, int64_t m, gn_ipm_vecs v, double mu, gn_vec7 pv, Bx bx) {
+  shift(v, bx);
+  shift(pv, bx);
+  mu = bpar(bx, GN_BP_MU, mu);
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
     const double wl = v.dxl[i], wu = v.dxu[i];
@@ -132,7 +145,11 @@ __device__ __forceinline__ double dftb1(double z, double dz, double tau) {
 }
 
 __global__ void __launch_bounds__(kRedThreads)
-direction_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double mu, double tau, RedSpec rs) {
+direction_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double mu, double tau, RedSpec rs, Bx bx) {
+  shift(v, bx);
+  shift(st, bx);
+  mu = bpar(bx, GN_BP_MU, mu);
+  tau = bpar(bx, GN_BP_TAU, tau);
   double acc[4] = {1.0, 1.0, 1.0, 0.0};
   const int64_t len = n > m ? n : m;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < len;
@@ -158,7 +175,12 @@ direction_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double mu, dou
 }
 
 __global__ void trial_point_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double alpha,
-                                   double *xt, double *s_t) {
+                                   double *xt, double *s_t, Bx bx) {
+  shift(v, bx);
+  shift(st, bx);
+  alpha = bpar(bx, GN_BP_ALPHA, alpha);
+  xt = shift_ptr(xt, n);
+  s_t = shift_ptr(s_t, m);
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) xt[i] = v.x[i] + alpha * st.x[i];
   if (i < m) s_t[i] = v.s[i] + alpha * st.s[i];
@@ -167,7 +189,12 @@ __global__ void trial_point_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 
 // first trial of the line search at alpha_max = min(alpha_x, alpha_s) read
 // from the device (Python's min(a0, a1)), so it needs no host round trip
 __global__ void trial_point_at_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st,
-                                      const double *alpha_pair, double *xt, double *s_t) {
+                                      const double *alpha_pair, double *xt, double *s_t, Bx bx) {
+  shift(v, bx);
+  shift(st, bx);
+  alpha_pair = shift_ptr(alpha_pair, GN_BATCH_SCAL);
+  xt = shift_ptr(xt, n);
+  s_t = shift_ptr(s_t, m);
   const double a0 = alpha_pair[0], a1 = alpha_pair[1];
   const double alpha = a1 < a0 ? a1 : a0;
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -177,7 +204,11 @@ __global__ void trial_point_at_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_ve
 
 __global__ void __launch_bounds__(kRedThreads)
 trial_merit_kernel(int64_t n, int64_t m, gn_ipm_vecs v, const double *ct, const double *xt,
-                   const double *s_t, RedSpec rs) {
+                   const double *s_t, RedSpec rs, Bx bx) {
+  shift(v, bx);
+  ct = shift_ptr(ct, m);
+  xt = shift_ptr(xt, n);
+  s_t = shift_ptr(s_t, m);
   double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const int64_t len = n > m ? n : m;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < len;
@@ -203,7 +234,14 @@ __device__ __forceinline__ double safeguard(double z, double w, double mu, doubl
 }
 
 __global__ void accept_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, double alpha, double az,
-                              double mu, double ks, int32_t *flags) {
+                              double mu, double ks, int32_t *flags, Bx bx) {
+  if (!b_active(bx)) return;
+  shift(v, bx);
+  shift(st, bx);
+  alpha = bpar(bx, GN_BP_ALPHA, alpha);
+  az = bpar(bx, GN_BP_ALPHA_Z, az);
+  mu = bpar(bx, GN_BP_MU, mu);
+  flags = shift_ptr(flags, 1);
   int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) {
     const double x = v.x[i] + alpha * st.x[i];
@@ -232,32 +270,50 @@ unsigned ew_blocks(int64_t len) { return static_cast<unsigned>(len > 0 ? (len + 
 using namespace gn;
 #define ST(s) static_cast<cudaStream_t>(s)
 
+namespace gn {
+void kkt_reserve(Kkt &K, int B, cudaStream_t st);   // kkt.cu
+namespace {
+dim3 bgrid(unsigned gx, int B) { return dim3(gx, static_cast<unsigned>(B), 1); }
+Bx bx_of(const Kkt &K, const double *bp) { return Bx{bp, K.n, K.m, K.nh, K.nj}; }
+
+void prep(Kkt &K, int B, const gn_ipm_vecs *v, int n_mu, const double *mus_host, const double *mus_dev,
+          const double *bp, double *scal, int64_t sstride, cudaStream_t s) {
+  GN_REQUIRE(n_mu >= 0 && n_mu <= GN_IPM_MAX_MU, "too many barrier candidates");
+  kkt_reserve(K, B, s);
+  MuList mus{};
+  mus.n = n_mu;
+  mus.dev = mus_dev;
+  if (mus_host)
+    for (int k = 0; k < n_mu; ++k) mus.mu[k] = mus_host[k];
+  int ops_x[4 + GN_IPM_MAX_MU] = {RED_MAX, RED_SUM, RED_SUM, RED_SUM};
+  for (int k = 0; k < n_mu; ++k) ops_x[4 + k] = RED_MAX;
+  int ops_s[7 + GN_IPM_MAX_MU] = {RED_MAX, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+  for (int k = 0; k < n_mu; ++k) ops_s[7 + k] = RED_MAX;
+  if (B == 1) {
+    GN_CUDA(cudaMemsetAsync(scal, 0, sizeof(double) * GN_PREP_DOUBLES, s));
+  } else {
+    GN_CUDA(cudaMemset2DAsync(scal, sizeof(double) * sstride, 0, sizeof(double) * GN_PREP_DOUBLES, B, s));
+  }
+  const Bx bx = bx_of(K, bp);
+  if (K.n)
+    GN_LAUNCH(prep_x_kernel, bgrid(red_grid(K.n), B), kRedThreads, 0, s, K.n, K.d.at_ptr, K.d.at_p, K.d.at_row,
+              *v, mus, spec(K, scal, 4 + n_mu, ops_x, sstride), bx);
+  if (K.m)
+    GN_LAUNCH(prep_s_kernel, bgrid(red_grid(K.m), B), kRedThreads, 0, s, K.m, *v, mus,
+              spec(K, scal + GN_PREP_S, 7 + n_mu, ops_s, sstride), bx);
+}
+}  // namespace
+}  // namespace gn
+
 extern "C" int gn_ipm_prep(gn_kkt *K, const gn_ipm_vecs *v, int32_t n_mu, const double *mus_host,
                            double *scal, void *stream) {
-  return guarded([&] {
-    GN_REQUIRE(n_mu >= 0 && n_mu <= GN_IPM_MAX_MU, "too many barrier candidates");
-    MuList mus{};
-    mus.n = n_mu;
-    for (int k = 0; k < n_mu; ++k) mus.mu[k] = mus_host[k];
-    int ops_x[4 + GN_IPM_MAX_MU] = {RED_MAX, RED_SUM, RED_SUM, RED_SUM};
-    for (int k = 0; k < n_mu; ++k) ops_x[4 + k] = RED_MAX;
-    int ops_s[7 + GN_IPM_MAX_MU] = {RED_MAX, RED_MAX, RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
-    for (int k = 0; k < n_mu; ++k) ops_s[7 + k] = RED_MAX;
-    GN_CUDA(cudaMemsetAsync(scal, 0, sizeof(double) * GN_PREP_DOUBLES, ST(stream)));
-    if (K->n)
-      GN_LAUNCH(prep_x_kernel, red_grid(K->n), kRedThreads, 0, ST(stream), 
-          K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *v, mus, spec(*K, scal, 4 + n_mu, ops_x));
-    if (K->m)
-      GN_LAUNCH(prep_s_kernel, red_grid(K->m), kRedThreads, 0, ST(stream), K->m, *v, mus,
-                                                                  spec(*K, scal + GN_PREP_S, 7 + n_mu, ops_s));
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { prep(*K, 1, v, n_mu, mus_host, nullptr, nullptr, scal, 0, ST(stream)); });
 }
 
 extern "C" int gn_ipm_pvec(gn_kkt *K, const gn_ipm_vecs *v, double mu, gn_vec7 *pv, void *stream) {
   return guarded([&] {
-    GN_LAUNCH(pvec_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, mu, *pv);
-    GN_LAUNCH_CHECK();
+    GN_LAUNCH(pvec_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, mu, *pv,
+              bx_of(*K, nullptr));
   });
 }
 
@@ -265,18 +321,16 @@ extern "C" int gn_ipm_direction(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *
                                 double *scal, void *stream) {
   return guarded([&] {
     int ops[4] = {RED_MIN, RED_MIN, RED_MIN, RED_SUM};
-    GN_LAUNCH(direction_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), 
-        K->n, K->m, *v, *steps, mu, tau, spec(*K, scal, 4, ops));
-    GN_LAUNCH_CHECK();
+    GN_LAUNCH(direction_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), K->n, K->m, *v,
+              *steps, mu, tau, spec(*K, scal, 4, ops), bx_of(*K, nullptr));
   });
 }
 
 extern "C" int gn_ipm_trial_point(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                                   double *xt, double *st, void *stream) {
   return guarded([&] {
-    GN_LAUNCH(trial_point_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps, alpha,
-                                                                               xt, st);
-    GN_LAUNCH_CHECK();
+    GN_LAUNCH(trial_point_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps,
+              alpha, xt, st, bx_of(*K, nullptr));
   });
 }
 
@@ -284,7 +338,7 @@ extern "C" int gn_ipm_trial_point_at(gn_kkt *K, const gn_ipm_vecs *v, const gn_v
                                      const double *alpha_pair, double *xt, double *st, void *stream) {
   return guarded([&] {
     GN_LAUNCH(trial_point_at_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v,
-              *steps, alpha_pair, xt, st);
+              *steps, alpha_pair, xt, st, bx_of(*K, nullptr));
   });
 }
 
@@ -292,9 +346,8 @@ extern "C" int gn_ipm_trial_merit(gn_kkt *K, const gn_ipm_vecs *v, const double 
                                   const double *st, double *scal, void *stream) {
   return guarded([&] {
     int ops[5] = {RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
-    GN_LAUNCH(trial_merit_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), 
-        K->n, K->m, *v, ct, xt, st, spec(*K, scal, 5, ops));
-    GN_LAUNCH_CHECK();
+    GN_LAUNCH(trial_merit_kernel, red_grid(std::max(K->n, K->m)), kRedThreads, 0, ST(stream), K->n, K->m, *v,
+              ct, xt, st, spec(*K, scal, 5, ops), bx_of(*K, nullptr));
   });
 }
 
@@ -302,7 +355,65 @@ extern "C" int gn_ipm_accept(gn_kkt *K, const gn_ipm_vecs *v, const gn_vec7 *ste
                              double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream) {
   return guarded([&] {
     GN_LAUNCH(accept_kernel, ew_blocks(std::max(K->n, K->m)), 256, 0, ST(stream), K->n, K->m, *v, *steps, alpha,
-                                                                          alpha_z, mu, kappa_sigma, flags);
-    GN_LAUNCH_CHECK();
+              alpha_z, mu, kappa_sigma, flags, bx_of(*K, nullptr));
+  });
+}
+
+// ----------------------------------------------------------- batched (K12)
+// bp: [B][GN_BP_STRIDE] per-instance operands; scal: [B][GN_BATCH_SCAL]
+extern "C" int gn_ipm_prep_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, int32_t n_mu, const double *mus_dev,
+                                   double *scal, void *stream) {
+  return guarded([&] { prep(*K, B, v, n_mu, nullptr, mus_dev, nullptr, scal, GN_BATCH_SCAL, ST(stream)); });
+}
+
+extern "C" int gn_ipm_pvec_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const double *bp, gn_vec7 *pv,
+                                   void *stream) {
+  return guarded([&] {
+    GN_LAUNCH(pvec_kernel, bgrid(ew_blocks(std::max(K->n, K->m)), B), 256, 0, ST(stream), K->n, K->m, *v, 0.0,
+              *pv, bx_of(*K, bp));
+  });
+}
+
+extern "C" int gn_ipm_direction_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                        const double *bp, double *scal, void *stream) {
+  return guarded([&] {
+    kkt_reserve(*K, B, ST(stream));
+    int ops[4] = {RED_MIN, RED_MIN, RED_MIN, RED_SUM};
+    GN_LAUNCH(direction_kernel, bgrid(red_grid(std::max(K->n, K->m)), B), kRedThreads, 0, ST(stream), K->n, K->m,
+              *v, *steps, 0.0, 0.0, spec(*K, scal, 4, ops, GN_BATCH_SCAL), bx_of(*K, bp));
+  });
+}
+
+extern "C" int gn_ipm_trial_point_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                          const double *bp, double *xt, double *st, void *stream) {
+  return guarded([&] {
+    GN_LAUNCH(trial_point_kernel, bgrid(ew_blocks(std::max(K->n, K->m)), B), 256, 0, ST(stream), K->n, K->m, *v,
+              *steps, 0.0, xt, st, bx_of(*K, bp));
+  });
+}
+
+extern "C" int gn_ipm_trial_point_at_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                             const double *alpha_pairs, double *xt, double *st, void *stream) {
+  return guarded([&] {
+    GN_LAUNCH(trial_point_at_kernel, bgrid(ew_blocks(std::max(K->n, K->m)), B), 256, 0, ST(stream), K->n, K->m,
+              *v, *steps, alpha_pairs, xt, st, bx_of(*K, nullptr));
+  });
+}
+
+extern "C" int gn_ipm_trial_merit_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const double *ct,
+                                          const double *xt, const double *st, double *scal, void *stream) {
+  return guarded([&] {
+    kkt_reserve(*K, B, ST(stream));
+    int ops[5] = {RED_SUM, RED_SUM, RED_SUM, RED_SUM, RED_SUM};
+    GN_LAUNCH(trial_merit_kernel, bgrid(red_grid(std::max(K->n, K->m)), B), kRedThreads, 0, ST(stream), K->n,
+              K->m, *v, ct, xt, st, spec(*K, scal, 5, ops, GN_BATCH_SCAL), bx_of(*K, nullptr));
+  });
+}
+
+extern "C" int gn_ipm_accept_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v, const gn_vec7 *steps,
+                                     const double *bp, double kappa_sigma, int32_t *flags, void *stream) {
+  return guarded([&] {
+    GN_LAUNCH(accept_kernel, bgrid(ew_blocks(std::max(K->n, K->m)), B), 256, 0, ST(stream), K->n, K->m, *v,
+              *steps, 0.0, 0.0, 0.0, kappa_sigma, flags, bx_of(*K, bp));
   });
 }

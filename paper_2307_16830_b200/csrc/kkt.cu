@@ -113,9 +113,11 @@ __global__ void at_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *p
 
 // D = (Sigma_s + dw) C, C = 1 / (dc Sigma_s + (1 + dc dw)) per row
 // (kkt.py:153-157), once per row instead of once per product
-__global__ void d_rows_kernel(int64_t m, gn_kkt_state st, double *d) {
+__global__ void d_rows_kernel(int64_t m, gn_kkt_state st, double *d, Bx bx) {
   int64_t r = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (r >= m) return;
+  shift(st, bx);
+  d = shift_ptr(d, m);
   const double ssr = st.ss[r];
   const double cfac = __dadd_rn(1.0, __dmul_rn(st.dc, st.dw));
   const double c = 1.0 / __dadd_rn(__dmul_rn(st.dc, ssr), cfac);
@@ -130,9 +132,12 @@ __global__ void __launch_bounds__(kT)
 assemble_kernel(int64_t nk, const int32_t *__restrict__ kp, const int32_t *__restrict__ krow,
                 const int32_t *__restrict__ ks1, const int32_t *__restrict__ ks2,
                 const int32_t *__restrict__ kw, const int32_t *__restrict__ kd, gn_kkt_state st,
-                const double *__restrict__ d, double *K) {
+                const double *__restrict__ d, double *K, Bx bx) {
   int64_t s = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (s >= nk) return;
+  shift(st, bx);
+  d = shift_ptr(d, bx.m);
+  K = shift_ptr(K, nk);
   const int p0 = __ldg(kp + s), p1 = __ldg(kp + s + 1);
   const int w = __ldg(kw + s), dg = __ldg(kd + s);
   double acc = 0.0;
@@ -166,9 +171,15 @@ __device__ __forceinline__ double c_of(const gn_kkt_state &st, double ssr) {
 }
 
 // m-side of the condensed rhs: qs, qy and u = C qs + D qy
-__global__ void rhs_rows_kernel(int64_t m, gn_kkt_state st, gn_vec7 pv, double *qs, double *qy, double *u) {
+__global__ void rhs_rows_kernel(int64_t m, gn_kkt_state st, gn_vec7 pv, double *qs, double *qy, double *u,
+                                Bx bx) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= m) return;
+  shift(st, bx);
+  shift(pv, bx);
+  qs = shift_ptr(qs, m);
+  qy = shift_ptr(qy, m);
+  u = shift_ptr(u, m);
   const double q_s = __dsub_rn(__dadd_rn(pv.s[i], __dmul_rn(inv_or_zero(st.dsl[i]), pv.zsl[i])),
                                __dmul_rn(inv_or_zero(st.dsu[i]), pv.zsu[i]));
   const double q_y = pv.y[i];
@@ -181,9 +192,14 @@ __global__ void rhs_rows_kernel(int64_t m, gn_kkt_state st, gn_vec7 pv, double *
 
 // n-side: qx and rhs = qx + A^T u
 __global__ void rhs_cols_kernel(int64_t n, const int64_t *ptr, const int32_t *pp, const int32_t *row,
-                                gn_kkt_state st, gn_vec7 pv, const double *u, double *qx, double *rhs) {
+                                gn_kkt_state st, gn_vec7 pv, const double *u, double *qx, double *rhs, Bx bx) {
   int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (j >= n) return;
+  shift(st, bx);
+  shift(pv, bx);
+  u = shift_ptr(u, bx.m);
+  qx = shift_ptr(qx, n);
+  rhs = shift_ptr(rhs, n);
   const double q_x = __dsub_rn(__dadd_rn(pv.x[j], __dmul_rn(inv_or_zero(st.dxl[j]), pv.zxl[j])),
                                __dmul_rn(inv_or_zero(st.dxu[j]), pv.zxu[j]));
   const double acc = gather_dot(ptr[j], ptr[j + 1], st.a, [&](int64_t t) { return pp[t]; }, u,
@@ -194,9 +210,15 @@ __global__ void rhs_cols_kernel(int64_t n, const int64_t *ptr, const int32_t *pp
 
 __global__ void recover_sd_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, gn_kkt_state st,
                                   const double *dx, const double *qs, const double *qy, double *ds,
-                                  double *dy) {
+                                  double *dy, Bx bx) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= m) return;
+  shift(st, bx);
+  dx = shift_ptr(dx, bx.n);
+  qs = shift_ptr(qs, m);
+  qy = shift_ptr(qy, m);
+  ds = shift_ptr(ds, m);
+  dy = shift_ptr(dy, m);
   const double ax = gather_dot(rowptr[i], rowptr[i + 1], st.a, [](int64_t p) { return p; }, dx,
                                [&](int64_t p) { return col[p]; });
   const double c = c_of(st, st.ss[i]);
@@ -210,6 +232,10 @@ __global__ void recover_bd_kernel(int64_t len, const double *dl, const double *d
                                   double *dzl, double *dzu, int32_t *flags) {
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i >= len) return;
+  // batched: every array is [B][len], flags [B]
+  dl = shift_ptr(dl, len); du = shift_ptr(du, len); zl = shift_ptr(zl, len); zu = shift_ptr(zu, len);
+  pzl = shift_ptr(pzl, len); pzu = shift_ptr(pzu, len); dv = shift_ptr(dv, len);
+  dzl = shift_ptr(dzl, len); dzu = shift_ptr(dzu, len); flags = shift_ptr(flags, 1);
   const double wl = dl[i], wu = du[i];
   if ((isfinite(wl) && !(wl > 0.0)) || (isfinite(wu) && !(wu > 0.0))) atomicOr(flags, 1);
   dzl[i] = __dmul_rn(inv_or_zero(wl), __dsub_rn(pzl[i], __dmul_rn(zl[i], dv[i])));
@@ -219,7 +245,11 @@ __global__ void recover_bd_kernel(int64_t len, const double *dl, const double *d
 // x-side residual blocks in double-double: rx, rzxl, rzxu (kkt.py:199-206)
 __global__ void residual_x_kernel(int64_t n, const int64_t *wptr, const int32_t *wp, const int32_t *wj,
                                   const int64_t *atptr, const int32_t *atp, const int32_t *atrow,
-                                  gn_kkt_state st, gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs) {
+                                  gn_kkt_state st, gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs, Bx bx) {
+  shift(st, bx);
+  shift(step, bx);
+  shift(pv, bx);
+  shift(res, bx);
   double vmax[1] = {0.0};
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; j < n;
        j += static_cast<int64_t>(gridDim.x) * kT) {
@@ -252,7 +282,11 @@ __global__ void residual_x_kernel(int64_t n, const int64_t *wptr, const int32_t 
 
 // s/y-side residual blocks: rs, ry, rzsl, rzsu (kkt.py:202-208)
 __global__ void residual_s_kernel(int64_t m, const int64_t *rowptr, const int32_t *col, gn_kkt_state st,
-                                  gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs) {
+                                  gn_vec7 step, gn_vec7 pv, gn_vec7 res, RedSpec rs, Bx bx) {
+  shift(st, bx);
+  shift(step, bx);
+  shift(pv, bx);
+  shift(res, bx);
   double vmax[1] = {0.0};
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; i < m;
        i += static_cast<int64_t>(gridDim.x) * kT) {
@@ -283,13 +317,18 @@ __global__ void residual_s_kernel(int64_t m, const int64_t *rowptr, const int32_
   grid_reduce<1>(rs, vmax);
 }
 
-__global__ void max2_kernel(const double *a, const double *b, double *out) {
-  double x = *a, y = *b;
-  *out = (x != x) ? x : ((y != y) ? y : fmax(x, y));
+// out[i * stride] = max(a[i * stride], b[i * stride]) for every instance i
+__global__ void max2_kernel(const double *a, const double *b, double *out, int B, int64_t stride) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= B) return;
+  double x = a[i * stride], y = b[i * stride];
+  out[i * stride] = (x != x) ? x : ((y != y) ? y : fmax(x, y));
 }
 
 // max over |w|, |a|, |Sigma|, |z|, finite widths (kkt.py:211-221)
-__global__ void matrix_scale_kernel(int64_t n, int64_t m, int64_t nh, int64_t nj, gn_kkt_state st, RedSpec rs) {
+__global__ void matrix_scale_kernel(int64_t n, int64_t m, int64_t nh, int64_t nj, gn_kkt_state st, RedSpec rs,
+                                    Bx bx) {
+  shift(st, bx);
   double v[1] = {1.0};
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -310,7 +349,13 @@ __global__ void matrix_scale_kernel(int64_t n, int64_t m, int64_t nh, int64_t nj
   grid_reduce<1>(rs, v);
 }
 
-__global__ void axpy7_kernel(int64_t n, int64_t m, gn_vec7 y, gn_vec7 x, double alpha) {
+__global__ void axpy7_kernel(int64_t n, int64_t m, gn_vec7 y, gn_vec7 x, double alpha, Bx bx) {
+  if (bx.bp) {   // batched: per-instance alpha (0 leaves an instance unchanged)
+    alpha = bpar(bx, GN_BP_ALPHA, alpha);
+    if (alpha == 0.0) return;
+    shift(y, bx);
+    shift(x, bx);
+  }
   int64_t i = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   if (i < n) {
     y.x[i] += alpha * x.x[i];
@@ -325,15 +370,19 @@ __global__ void axpy7_kernel(int64_t n, int64_t m, gn_vec7 y, gn_vec7 x, double 
   }
 }
 
-RedSpec max_spec(Kkt &K, double *out) {
+RedSpec max_spec(Kkt &K, double *out, int64_t out_stride = 0) {
   RedSpec r{};
   r.k = 1;
   r.op[0] = RED_MAX;
   r.out = out;
   r.partials = K.d.partials;
   r.counter = K.d.counter;
+  r.out_stride = out_stride;
   return r;
 }
+
+Bx single(const Kkt &K) { return Bx{nullptr, K.n, K.m, K.nh, K.nj}; }
+Bx batched(const Kkt &K, const double *bp) { return Bx{bp, K.n, K.m, K.nh, K.nj}; }
 
 }  // namespace
 
@@ -401,6 +450,7 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
   GN_CUDA(cudaMemset(K.d.counter, 0, sizeof(unsigned int)));
   K.d.scratch = dev_alloc<double>(m > 0 ? m : 1);
   K.d.dvec = dev_alloc<double>(m > 0 ? m : 1);
+  K.batch_cap = 1;
   if (cs) {
     GN_REQUIRE(cs->n == n && cs->nnz_h == nh && cs->nnz_j == nj, "condensed structure mismatch");
     const_cast<Condense *>(cs)->ensure_assembly_plan();
@@ -447,12 +497,112 @@ extern "C" int gn_kkt_create(int64_t n, int64_t m, int64_t nh, const int64_t *hr
 
 extern "C" void gn_kkt_destroy(gn_kkt *K) { delete K; }
 
+namespace gn {
+// Scratch of batched launches: reduction partials/counters and the m-vectors
+// (condensed-rhs u, assembly D) for B instances; grown on demand.  The
+// stream is synchronised before a buffer is replaced (queued work may still
+// read the old one).
+void kkt_reserve(Kkt &K, int B, cudaStream_t st) {
+  const int64_t blocks = static_cast<int64_t>(B) * kRedMaxBlocks;
+  if (B <= K.batch_cap) return;
+  GN_CUDA(cudaStreamSynchronize(st));
+  dev_free(K.d.partials);
+  dev_free(K.d.counter);
+  dev_free(K.d.scratch);
+  dev_free(K.d.dvec);
+  K.d.partials = dev_alloc<double>(blocks * kRedMaxSlots);
+  K.d.counter = dev_alloc<unsigned int>(B);
+  GN_CUDA(cudaMemset(K.d.counter, 0, sizeof(unsigned int) * B));
+  K.d.scratch = dev_alloc<double>(K.m > 0 ? K.m * B : 1);
+  K.d.dvec = dev_alloc<double>(K.m > 0 ? K.m * B : 1);
+  K.batch_cap = B;
+}
+
+namespace {
+dim3 bgrid(unsigned gx, int B) { return dim3(gx, static_cast<unsigned>(B), 1); }
+
+void assemble(Kkt &K, int B, const gn_kkt_state *st, const double *bp, double *kvals, cudaStream_t s) {
+  GN_REQUIRE(K.has_assembly, "KKT plan built without the condensed structure");
+  if (K.nk == 0) return;
+  kkt_reserve(K, B, s);
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  if (K.m) GN_LAUNCH(d_rows_kernel, bgrid(blocks_for(K.m), B), kT, 0, s, K.m, *st, K.d.dvec, bx);
+  GN_LAUNCH(assemble_kernel, bgrid(blocks_for(K.nk), B), kT, 0, s, K.nk, K.d.k_ptr, K.d.k_row, K.d.k_s1,
+            K.d.k_s2, K.d.k_w, K.d.k_diag, *st, K.d.dvec, kvals, bx);
+}
+
+void condense_rhs(Kkt &K, int B, const gn_kkt_state *st, const double *bp, const gn_vec7 *pv, double *qx,
+                  double *qs, double *qy, double *rhs, cudaStream_t s) {
+  kkt_reserve(K, B, s);
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  if (K.m)
+    GN_LAUNCH(rhs_rows_kernel, bgrid(blocks_for(K.m), B), kT, 0, s, K.m, *st, *pv, qs, qy, K.d.scratch, bx);
+  if (K.n)
+    GN_LAUNCH(rhs_cols_kernel, bgrid(blocks_for(K.n), B), kT, 0, s, K.n, K.d.at_ptr, K.d.at_p, K.d.at_row, *st,
+              *pv, K.d.scratch, qx, rhs, bx);
+}
+
+void recover_sd(Kkt &K, int B, const gn_kkt_state *st, const double *bp, const double *dx, const double *qs,
+                const double *qy, double *ds, double *dy, cudaStream_t s) {
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  if (K.m)
+    GN_LAUNCH(recover_sd_kernel, bgrid(blocks_for(K.m), B), kT, 0, s, K.m, K.d.a_rowptr, K.d.a_col, *st, dx, qs,
+              qy, ds, dy, bx);
+}
+
+void recover_bd(Kkt &K, int B, const gn_kkt_state *st, const double *dx, const double *ds, const gn_vec7 *pv,
+                double *dzxl, double *dzxu, double *dzsl, double *dzsu, int32_t *flags, cudaStream_t s) {
+  if (K.n)
+    GN_LAUNCH(recover_bd_kernel, bgrid(blocks_for(K.n), B), kT, 0, s, K.n, st->dxl, st->dxu, st->zxl, st->zxu,
+              pv->zxl, pv->zxu, dx, dzxl, dzxu, flags);
+  if (K.m)
+    GN_LAUNCH(recover_bd_kernel, bgrid(blocks_for(K.m), B), kT, 0, s, K.m, st->dsl, st->dsu, st->zsl, st->zsu,
+              pv->zsl, pv->zsu, ds, dzsl, dzsu, flags);
+}
+
+// norm[b * stride + 0] = residual max of instance b (norm[.. + 1] scratch)
+void residual(Kkt &K, int B, const gn_kkt_state *st, const double *bp, const gn_vec7 *steps, const gn_vec7 *pv,
+              gn_vec7 *res, double *norm, int64_t stride, cudaStream_t s) {
+  kkt_reserve(K, B, s);
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  RedSpec rx = max_spec(K, norm, stride);
+  if (K.n)
+    GN_LAUNCH(residual_x_kernel, bgrid(red_grid(K.n), B), kRedThreads, 0, s, K.n, K.d.w_ptr, K.d.w_p, K.d.w_j,
+              K.d.at_ptr, K.d.at_p, K.d.at_row, *st, *steps, *pv, *res, rx, bx);
+  else
+    GN_CUDA(cudaMemsetAsync(norm, 0, sizeof(double), s));   // single instance only
+  RedSpec rs = max_spec(K, norm + 1, stride);
+  if (K.m)
+    GN_LAUNCH(residual_s_kernel, bgrid(red_grid(K.m), B), kRedThreads, 0, s, K.m, K.d.a_rowptr, K.d.a_col, *st,
+              *steps, *pv, *res, rs, bx);
+  else
+    GN_CUDA(cudaMemsetAsync(norm + 1, 0, sizeof(double), s));
+  GN_LAUNCH(max2_kernel, (B + 127) / 128, 128, 0, s, norm, norm + 1, norm, B, stride);
+}
+
+void matrix_scale(Kkt &K, int B, const gn_kkt_state *st, const double *bp, double *out, int64_t stride,
+                  cudaStream_t s) {
+  kkt_reserve(K, B, s);
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  int64_t big = std::max(std::max(K.n, K.m), std::max(K.nh, K.nj));
+  RedSpec r = max_spec(K, out, stride);
+  GN_LAUNCH(matrix_scale_kernel, bgrid(red_grid(big, 4), B), kRedThreads, 0, s, K.n, K.m, K.nh, K.nj, *st, r, bx);
+}
+
+void axpy7(Kkt &K, int B, gn_vec7 *y, const gn_vec7 *x, double alpha, const double *bp, cudaStream_t s) {
+  int64_t len = std::max(K.n, K.m);
+  if (len == 0) return;
+  const Bx bx = bp ? batched(K, bp) : single(K);
+  GN_LAUNCH(axpy7_kernel, bgrid(blocks_for(len), B), kT, 0, s, K.n, K.m, *y, *x, alpha, bx);
+}
+}  // namespace
+}  // namespace gn
+
 extern "C" int gn_kkt_sigma(int64_t len, const double *dl, const double *du, const double *zl,
                             const double *zu, double *sigma, void *stream) {
   return guarded([&] {
     if (len == 0) return;
     GN_LAUNCH(sigma_kernel, blocks_for(len), kT, 0, ST(stream), len, dl, du, zl, zu, sigma);
-    GN_LAUNCH_CHECK();
   });
 }
 
@@ -465,19 +615,11 @@ extern "C" int gn_kkt_matvec(gn_kkt *K, int kind, const double *vals, const doub
       GN_LAUNCH(a_matvec_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, vals, v, out);
     else if (kind == 2 && K->n)
       GN_LAUNCH(at_matvec_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, vals, v, out);
-    GN_LAUNCH_CHECK();
   });
 }
 
 extern "C" int gn_kkt_assemble(gn_kkt *K, const gn_kkt_state *st, double *kvals, void *stream) {
-  return guarded([&] {
-    GN_REQUIRE(K->has_assembly, "KKT plan built without the condensed structure");
-    if (K->nk == 0) return;
-    if (K->m) GN_LAUNCH(d_rows_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, *st, K->d.dvec);
-    GN_LAUNCH(assemble_kernel, blocks_for(K->nk), kT, 0, ST(stream), K->nk, K->d.k_ptr, K->d.k_row, K->d.k_s1,
-              K->d.k_s2, K->d.k_w, K->d.k_diag, *st, K->d.dvec, kvals);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { assemble(*K, 1, st, nullptr, kvals, ST(stream)); });
 }
 
 extern "C" int gn_kkt_assembly_traffic(const gn_kkt *K, int64_t *bytes) {
@@ -491,76 +633,73 @@ extern "C" int gn_kkt_assembly_traffic(const gn_kkt *K, int64_t *bytes) {
 
 extern "C" int gn_kkt_condense_rhs(gn_kkt *K, const gn_kkt_state *st, const gn_vec7 *pv, double *qx,
                                    double *qs, double *qy, double *rhs, void *stream) {
-  return guarded([&] {
-    if (K->m)
-      GN_LAUNCH(rhs_rows_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, *st, *pv, qs, qy, K->d.scratch);
-    if (K->n)
-      GN_LAUNCH(rhs_cols_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, K->d.at_ptr, K->d.at_p, K->d.at_row, *st, *pv,
-                                                             K->d.scratch, qx, rhs);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { condense_rhs(*K, 1, st, nullptr, pv, qx, qs, qy, rhs, ST(stream)); });
 }
 
 extern "C" int gn_kkt_recover_slack_dual(gn_kkt *K, const gn_kkt_state *st, const double *dx,
                                          const double *qs, const double *qy, double *ds, double *dy,
                                          void *stream) {
-  return guarded([&] {
-    if (K->m)
-      GN_LAUNCH(recover_sd_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, *st, dx, qs, qy,
-                                                               ds, dy);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { recover_sd(*K, 1, st, nullptr, dx, qs, qy, ds, dy, ST(stream)); });
 }
 
 extern "C" int gn_kkt_recover_bound_duals(gn_kkt *K, const gn_kkt_state *st, const double *dx,
                                           const double *ds, const gn_vec7 *pv, double *dzxl, double *dzxu,
                                           double *dzsl, double *dzsu, int32_t *flags, void *stream) {
-  return guarded([&] {
-    if (K->n)
-      GN_LAUNCH(recover_bd_kernel, blocks_for(K->n), kT, 0, ST(stream), K->n, st->dxl, st->dxu, st->zxl, st->zxu, pv->zxl,
-                                                               pv->zxu, dx, dzxl, dzxu, flags);
-    if (K->m)
-      GN_LAUNCH(recover_bd_kernel, blocks_for(K->m), kT, 0, ST(stream), K->m, st->dsl, st->dsu, st->zsl, st->zsu, pv->zsl,
-                                                               pv->zsu, ds, dzsl, dzsu, flags);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { recover_bd(*K, 1, st, dx, ds, pv, dzxl, dzxu, dzsl, dzsu, flags, ST(stream)); });
 }
 
 extern "C" int gn_kkt_residual(gn_kkt *K, const gn_kkt_state *st, const gn_vec7 *steps, const gn_vec7 *pv,
                                gn_vec7 *res, double *norm, void *stream) {
-  return guarded([&] {
-    // norm[0..2): per-side maxima, combined into norm[0]
-    RedSpec rx = max_spec(*K, norm);
-    if (K->n)
-      GN_LAUNCH(residual_x_kernel, red_grid(K->n), kRedThreads, 0, ST(stream), K->n, K->d.w_ptr, K->d.w_p, K->d.w_j, K->d.at_ptr,
-                                                               K->d.at_p, K->d.at_row, *st, *steps, *pv, *res, rx);
-    else
-      GN_CUDA(cudaMemsetAsync(norm, 0, sizeof(double), ST(stream)));
-    RedSpec rs = max_spec(*K, norm + 1);
-    if (K->m)
-      GN_LAUNCH(residual_s_kernel, red_grid(K->m), kRedThreads, 0, ST(stream), K->m, K->d.a_rowptr, K->d.a_col, *st, *steps, *pv,
-                                                               *res, rs);
-    else
-      GN_CUDA(cudaMemsetAsync(norm + 1, 0, sizeof(double), ST(stream)));
-    GN_LAUNCH(max2_kernel, 1, 1, 0, ST(stream), norm, norm + 1, norm);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { residual(*K, 1, st, nullptr, steps, pv, res, norm, 0, ST(stream)); });
 }
 
 extern "C" int gn_kkt_matrix_scale(gn_kkt *K, const gn_kkt_state *st, double *out, void *stream) {
-  return guarded([&] {
-    int64_t big = std::max(std::max(K->n, K->m), std::max(K->nh, K->nj));
-    RedSpec r = max_spec(*K, out);
-    GN_LAUNCH(matrix_scale_kernel, red_grid(big, 4), kRedThreads, 0, ST(stream), K->n, K->m, K->nh, K->nj, *st, r);
-    GN_LAUNCH_CHECK();
-  });
+  return guarded([&] { matrix_scale(*K, 1, st, nullptr, out, 0, ST(stream)); });
 }
 
 extern "C" int gn_vec7_axpy(gn_kkt *K, gn_vec7 *y, const gn_vec7 *x, double alpha, void *stream) {
+  return guarded([&] { axpy7(*K, 1, y, x, alpha, nullptr, ST(stream)); });
+}
+
+// ----------------------------------------------------------- batched (K12)
+extern "C" int gn_kkt_assemble_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *bp,
+                                       double *kvals, void *stream) {
+  return guarded([&] { assemble(*K, B, st, bp, kvals, ST(stream)); });
+}
+
+extern "C" int gn_kkt_condense_rhs_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *bp,
+                                           const gn_vec7 *pv, double *qx, double *qs, double *qy, double *rhs,
+                                           void *stream) {
+  return guarded([&] { condense_rhs(*K, B, st, bp, pv, qx, qs, qy, rhs, ST(stream)); });
+}
+
+extern "C" int gn_kkt_recover_slack_dual_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *bp,
+                                                 const double *dx, const double *qs, const double *qy, double *ds,
+                                                 double *dy, void *stream) {
+  return guarded([&] { recover_sd(*K, B, st, bp, dx, qs, qy, ds, dy, ST(stream)); });
+}
+
+extern "C" int gn_kkt_recover_bound_duals_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *dx,
+                                                  const double *ds, const gn_vec7 *pv, double *dzxl, double *dzxu,
+                                                  double *dzsl, double *dzsu, int32_t *flags, void *stream) {
+  return guarded([&] { recover_bd(*K, B, st, dx, ds, pv, dzxl, dzxu, dzsl, dzsu, flags, ST(stream)); });
+}
+
+extern "C" int gn_kkt_residual_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *bp,
+                                       const gn_vec7 *steps, const gn_vec7 *pv, gn_vec7 *res, double *norm,
+                                       void *stream) {
+  return guarded([&] { residual(*K, B, st, bp, steps, pv, res, norm, GN_BATCH_SCAL, ST(stream)); });
+}
+
+extern "C" int gn_kkt_matrix_scale_batched(gn_kkt *K, int32_t B, const gn_kkt_state *st, const double *bp,
+                                           double *out, void *stream) {
+  return guarded([&] { matrix_scale(*K, B, st, bp, out, GN_BATCH_SCAL, ST(stream)); });
+}
+
+extern "C" int gn_vec7_axpy_batched(gn_kkt *K, int32_t B, gn_vec7 *y, const gn_vec7 *x, const double *bp,
+                                    void *stream) {
   return guarded([&] {
-    int64_t len = std::max(K->n, K->m);
-    if (len == 0) return;
-    GN_LAUNCH(axpy7_kernel, blocks_for(len), kT, 0, ST(stream), K->n, K->m, *y, *x, alpha);
-    GN_LAUNCH_CHECK();
+    GN_REQUIRE(bp != nullptr, "batched axpy needs the per-instance alpha array");
+    axpy7(*K, B, y, x, 0.0, bp, ST(stream));
   });
 }

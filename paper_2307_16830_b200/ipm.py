@@ -312,6 +312,49 @@ class _DeviceSolve:
         return self.host[lo:hi].numpy(), int(self.host_flags[0]), int(self.host_flags[1])
 
 
+def _plan_lookup(model, ordering):
+    """The cached symbolic plans of `model` for `ordering`, or a started host
+    analysis.  Keyed on the ordering's CONTENT (a copy is kept): a new array
+    that reuses a freed one's id, or one mutated in place, is a different
+    key.  Returns (key, analysis or None on a hit)."""
+    key = None if ordering is None else np.array(ordering, dtype=np.int64, copy=True)
+    cache = getattr(model, "_kkt_cache", None)
+    hit = cache is not None and ((cache[0] is None and key is None) or (
+        cache[0] is not None and key is not None and cache[0].shape == key.shape
+        and np.array_equal(cache[0], key)))
+    return key, (None if hit else HostAnalysis(model, ordering))
+
+
+def _plan_finish(model, key, analysis, setup):
+    """KKT workspace + condensed backend (device plans) of the analysis, or
+    the cached ones; cached on the model."""
+    if analysis is None:
+        _, ws, backend = model._kkt_cache
+        return ws, backend
+    n, m = model.n_var, model.n_con
+    t0 = time.perf_counter()
+    cs = analysis.condensed()
+    setup["wait_condense"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols,
+                      condensed=cs)
+    setup["kkt_workspace"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    sym = analysis.symbolic()
+    setup["wait_symbolic"] = time.perf_counter() - t0
+    backend = CondensedBackend(ws, timings=setup, structure=cs, symbolic=sym)
+    setup.update({"worker_" + k: v for k, v in analysis.timings.items()})
+    model._kkt_cache = (key, ws, backend)
+    return ws, backend
+
+
+def plans(model, ordering=None):
+    """(KKTWorkspace, CondensedBackend) of a model: the symbolic analysis and
+    device plans, computed once per sparsity pattern and ordering."""
+    key, analysis = _plan_lookup(model, ordering)
+    return _plan_finish(model, key, analysis, {})
+
+
 def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -> SolveReport:
     """Solve min f s.t. g in ranges, bounds -- on the GPU (ipm.py:301-563)."""
     opts = options if options is not None else SolverOptions()
@@ -321,14 +364,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     # symbolic analysis (condensed pattern, ordering, symbolic factor, device
     # plans) is a function of the sparsity only: cached on the model.  On a
     # miss its host part starts on a worker thread right away.
-    # keyed on the ordering's CONTENT (a copy is kept): a new array that
-    # reuses a freed one's id, or one mutated in place, is a different key
-    key = None if opts.ordering is None else np.array(opts.ordering, dtype=np.int64, copy=True)
-    cache = getattr(model, "_kkt_cache", None)
-    hit = cache is not None and ((cache[0] is None and key is None) or (
-        cache[0] is not None and key is not None and cache[0].shape == key.shape
-        and np.array_equal(cache[0], key)))
-    analysis = None if hit else HostAnalysis(model, opts.ordering)
+    key, analysis = _plan_lookup(model, opts.ordering)
     try:
         P = _DeviceSolve(model, opts, constraint_ranges)
         setup["problem"] = time.perf_counter() - t_start
@@ -344,23 +380,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     stream = D.stream_ptr()
     timer = _Timer()
 
-    if analysis is not None:
-        t0 = time.perf_counter()
-        cs = analysis.condensed()
-        setup["wait_condense"] = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        ws = KKTWorkspace(n, m, model.hess_rows, model.hess_cols, model.jac_rows, model.jac_cols,
-                          condensed=cs)
-        setup["kkt_workspace"] = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        sym = analysis.symbolic()
-        setup["wait_symbolic"] = time.perf_counter() - t0
-        backend = CondensedBackend(ws, timings=setup, structure=cs, symbolic=sym)
-        setup.update({"worker_" + k: v for k, v in analysis.timings.items()})
-        model._kkt_cache = (key, ws, backend)
-    else:
-        _, ws, backend = cache
-        backend.n_factorizations = 0
+    ws, backend = _plan_finish(model, key, analysis, setup)
+    backend.n_factorizations = 0
     # the workspace reads the solver's duals in place (no copies per iteration)
     ws.zxl, ws.zxu, ws.zsl, ws.zsu = P.zxl, P.zxu, P.zsl, P.zsu
     ws.delta_w = ws.delta_c = 0.0

@@ -89,3 +89,72 @@ def test_concurrent_batch_is_bitwise_sequential():
     for a, b in zip(seq, con):
         assert a.status == b.status == "optimal" and a.iterations == b.iterations
         np.testing.assert_array_equal(a.x, b.x)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tiles,seeds", [(4, range(5)), (97, range(6))])
+def test_instance_batched_solve_is_bitwise_single(tiles, seeds):
+    """K12: ONE batched solve (one launch per kernel for all instances, shared
+    plans) gives every instance exactly the iterates of solving it alone:
+    same status, iteration count, per-iteration trace and x (bitwise)."""
+    from paper_2307_16830_b200 import SolverOptions, solve
+    from paper_2307_16830_b200.batch_ipm import solve_batched
+
+    opts = SolverOptions(tol=1e-6)
+    reps = solve_batched(B.perturbed_instances(tiles, list(seeds)), opts)
+    for am, r in zip(B.perturbed_instances(tiles, list(seeds)), reps):
+        alone = solve(am.model, opts, constraint_ranges=am.ranges)
+        assert r.status == alone.status == "optimal"
+        assert r.iterations == alone.iterations
+        assert r.trace == alone.trace
+        np.testing.assert_array_equal(r.x, alone.x)
+        assert r.objective == alone.objective
+        assert r.constraint_violation == alone.constraint_violation
+
+
+@pytest.mark.gpu
+def test_instance_batched_c5_matches_reference(end_to_end):
+    """The three C5 instances with reference goldens (make_golden.py), solved
+    inside one batch: objective 1e-6 relative, iterations +-2."""
+    from paper_2307_16830_b200 import SolverOptions
+    from paper_2307_16830_b200.batch_ipm import solve_batched
+
+    reps = solve_batched(B.perturbed_instances(97, [0, 1, 2]), SolverOptions(tol=1e-6))
+    for seed, r in enumerate(reps):
+        ref = end_to_end[f"C5s{seed}@1e-06"]
+        assert r.status == ref["status"] == "optimal"
+        assert r.objective == pytest.approx(ref["objective"], rel=1e-6)
+        assert abs(r.iterations - ref["iterations"]) <= 2
+
+
+@pytest.mark.gpu
+def test_instance_batched_regularization_and_masking():
+    """Instances that need the inertia correction (concave objective) and
+    instances that converge at different iterations, in one batch: every
+    instance equals its single solve (the delta_w schedule per instance, the
+    finished ones masked out of every state-changing kernel)."""
+    from paper_2307_16830_b200 import SolverOptions, solve
+    from paper_2307_16830_b200.batch_ipm import solve_batched
+    from paper_2307_16830_b200.expressions import param, var
+    from paper_2307_16830_b200.model import ModelBuilder
+
+    def model(w):
+        b = ModelBuilder()
+        b.add_variables(3, np.full(3, -1.0), np.full(3, 2.0), np.zeros(3))
+        b.add_objective(-(var(0) - param(0)) ** 2 + param(1) * var(0) * var(1),
+                        np.array([[0, 1], [1, 2], [2, 0]]), np.array([[0.3, w], [0.1, w], [-0.2, w]]))
+        b.add_constraints(var(0) + var(1) + var(2) - 1.0, np.array([[0, 1, 2]]), np.zeros((1, 0)))
+        return b.finalize()
+
+    ws = (0.5, -0.4, 0.1, 1.5)
+    opts = SolverOptions(tol=1e-8)
+    reps = solve_batched([(model(w), None) for w in ws], opts)
+    its = set()
+    for w, r in zip(ws, reps):
+        alone = solve(model(w), opts)
+        assert r.status == alone.status
+        assert r.iterations == alone.iterations
+        assert [t[6] for t in r.trace] == [t[6] for t in alone.trace]
+        np.testing.assert_array_equal(r.x, alone.x)
+        its.add(r.iterations)
+    assert any(t[6] > 0 for r in reps for t in r.trace)
