@@ -340,6 +340,119 @@ def run_batch(args):
     return 0
 
 
+
+def _dmma_peak():
+    """FP64 tensor-core (DMMA m8n8k4) peak measured live on this device."""
+    import ctypes as _ct
+
+    from paper_2307_16830_b200 import _lib
+    from paper_2307_16830_b200 import device as D
+
+    dmma = _ct.c_double()
+    _lib.check(_lib.lib().gn_measure_dmma_peak(_ct.byref(dmma), D.stream_ptr()))
+    return dmma.value
+
+
+def phase_rooflines(model, ws, info, phases, peak, dmma_peak):
+    """Per-kernel-group rooflines from the CUDA-event phase means (DESIGN.md
+    §4): AD full evaluation, condensed assembly and the triangular solves
+    against the HBM peak (compulsory bytes per launch / mean launch time),
+    the refactorisation's FP64 flops against the measured DMMA peak."""
+    import ctypes as _ct
+
+    from paper_2307_16830_b200 import _lib
+
+    def _bytes(fn, *a):
+        b = _ct.c_int64()
+        _lib.check(fn(*a, _ct.byref(b)))
+        return int(b.value)
+
+    out = {}
+    nnz_l, n = info["nnz_l"], model.n_var
+    for name, span_name, nbytes in (
+            ("ad_full (gn_ad_eval: pattern kernels + gather)", "ad_full",
+             _bytes(_lib.lib().gn_model_traffic, model.device_plan(), 31)),
+            ("assemble (gn_kkt_assemble)", "assemble",
+             _bytes(_lib.lib().gn_kkt_assembly_traffic, ws.handle)),
+            # L read by both sweeps (values 8 B + row index 4 B each), rhs in, x out
+            ("solve (gn_chol_solve: forward + backward sweeps)", "solve", 24 * nnz_l + 16 * n)):
+        ph = phases.get(span_name)
+        if ph and ph["count"]:
+            ach = nbytes / (ph["mean_ms"] * 1e-3) / 1e9
+            out[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "alg_bytes_per_launch": nbytes,
+                         "mean_launch_ms": ph["mean_ms"]}
+    ref = phases.get("refactor")
+    if ref and ref["count"]:
+        alg = 12 * info["nnz_a"] + 12 * nnz_l
+        ach = alg / (ref["mean_ms"] * 1e-3) / 1e9
+        out["refactor (compulsory bytes vs HBM)"] = {
+            "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "alg_bytes_per_launch": alg, "mean_launch_ms": ref["mean_ms"]}
+        if dmma_peak > 0:
+            tf = info["flops"] / (ref["mean_ms"] * 1e-3) / 1e12
+            out["refactor (FP64 flops vs DMMA peak)"] = {
+                "bound": "tensor", "achieved": tf, "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": tf / dmma_peak, "flops_per_launch": info["flops"],
+                "peak_kind": "measured (gn_measure_dmma_peak, m8n8k4 f64)",
+                "mean_launch_ms": ref["mean_ms"],
+                "note": "latency-bound: the elimination-tree critical path (dependent fronts and "
+                        "panels), not DMMA or HBM throughput, sets the time"}
+    return out
+
+
+def large_record(workload, tol, steps, peak, dmma_peak):
+    """Device-resident solves of a second, larger workload (C4: 78,484 buses,
+    BASELINE configs[3]) inside the default bench run: per-iteration phase
+    times and the same per-kernel rooflines, so the driver-run line carries
+    the 78k numbers and not only the L2-resident C3 ones."""
+    import torch
+
+    from paper_2307_16830_b200 import SolverOptions, profiling, solve
+
+    t0 = time.perf_counter()
+    am = build_model(workload)
+    model = am.model
+    opts = SolverOptions(tol=tol)
+    rep = solve(model, opts, constraint_ranges=am.ranges)   # plans + ordering (untimed)
+    setup_s = time.perf_counter() - t0
+    rep = solve(model, opts, constraint_ranges=am.ranges)   # warm-up
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    profiling.reset()
+    profiling.enable(True)
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep = solve(model, opts, constraint_ranges=am.ranges)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    profiling.enable(False)
+    phases = profiling.summary()
+    del flush
+    _, ws, backend = model._kkt_cache
+    info = backend.symbolic.info
+    iters = max(1, rep.iterations)
+    rec = {
+        "workload": workload_config(workload, tol, model.n_var, model.n_con)["workload"],
+        "value": float(np.mean(ms)) / 1e3, "unit": "s", "steps": steps,
+        "steps_s": [round(v / 1e3, 4) for v in ms],
+        "status": rep.status, "iterations": rep.iterations, "objective": rep.objective,
+        "structure": {"nnz_jac": model.nnz_jac, "nnz_hess": model.nnz_hess, "nnz_K": info["nnz_a"],
+                      "nnz_L": info["nnz_l"], "fronts": info["n_fronts"],
+                      "front_levels": info["n_levels"], "max_front": info.get("max_front")},
+        "per_iter_ms": {k: v["total_ms"] / (steps * iters) for k, v in phases.items()},
+        "per_launch_ms": {k: v["mean_ms"] for k, v in phases.items()},
+        "rooflines": phase_rooflines(model, ws, info, phases, peak, dmma_peak),
+        "setup_s_untimed": round(setup_s, 2),
+    }
+    model.release_device()
+    return rec
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -350,6 +463,8 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-large", action="store_true",
+                    help="skip the C4 (78,484-bus) sub-record of the default C3 line")
     ap.add_argument("--batch", type=int, default=256, help="C5: number of instances")
     ap.add_argument("--concurrency", type=int, default=2,
                     help="C5 concurrent mode: solves per GPU (host threads x CUDA streams)")
@@ -487,40 +602,8 @@ def main():
     ref = phases.get("refactor", {"mean_ms": float("nan"), "count": 0})
     achieved = alg_bytes / (ref["mean_ms"] * 1e-3) / 1e9 if ref["count"] else None
     per_iter = {k: v["total_ms"] / (args.steps * max(1, iters)) for k, v in phases.items()}
-    # secondary rooflines: AD (full evaluation) and the condensed assembly
-    import ctypes as _ct
-
-    def _bytes(fn, *a):
-        b = _ct.c_int64()
-        _lib.check(fn(*a, _ct.byref(b)))
-        return int(b.value)
-
-    secondary = {}
-    for name, span_name, nbytes in (
-            ("ad_full (gn_ad_eval: pattern kernels + gather)", "ad_full",
-             _bytes(_lib.lib().gn_model_traffic, model.device_plan(), 31)),
-            ("assemble (gn_kkt_assemble)", "assemble",
-             _bytes(_lib.lib().gn_kkt_assembly_traffic, ws.handle))):
-        ph = phases.get(span_name)
-        if ph and ph["count"]:
-            ach = nbytes / (ph["mean_ms"] * 1e-3) / 1e9
-            secondary[name] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                               "frac": ach / peak, "alg_bytes_per_launch": nbytes,
-                               "mean_launch_ms": ph["mean_ms"]}
-
-    # the dense supernode part of the refactorisation against the FP64
-    # tensor-core peak measured live on this device (DMMA probe kernel)
-    dmma = _ct.c_double()
-    _lib.check(_lib.lib().gn_measure_dmma_peak(_ct.byref(dmma), D.stream_ptr()))
-    if ref["count"] and dmma.value > 0:
-        tf = info["flops"] / (ref["mean_ms"] * 1e-3) / 1e12
-        secondary["refactor (FP64 flops vs DMMA peak)"] = {
-            "bound": "tensor", "achieved": tf, "peak": dmma.value, "unit": "TFLOP/s",
-            "frac": tf / dmma.value, "flops_per_launch": info["flops"],
-            "peak_kind": "measured (gn_measure_dmma_peak, m8n8k4 f64)",
-            "mean_launch_ms": ref["mean_ms"],
-            "note": "latency-bound: the elimination-tree critical path (dependent fronts and "
-                    "panels), not DMMA or HBM throughput, sets the time"}
+    dmma_peak = _dmma_peak()
+    secondary = phase_rooflines(model, ws, info, phases, peak, dmma_peak)
 
     # DRAM traffic of one refactorisation from the committed ncu capture of
     # the same kernels (profiles/, tools/profile_round.sh), C3 only
@@ -543,6 +626,14 @@ def main():
         except Exception as exc:  # never fail the bench line on the baseline leg
             cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
+    large = None
+    if args.workload == "C3" and world == 1 and not args.no_large:
+        try:
+            model.release_device()
+            large = large_record("C4", args.tol, 2, peak, dmma_peak)
+        except Exception as exc:  # never fail the bench line on the sub-record
+            large = {"workload": "C4", "failed": f"{type(exc).__name__}: {exc}"}
+
     line = {
         "metric": METRIC, "value": ms_per_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -561,6 +652,7 @@ def main():
                      "mean_launch_ms": ref["mean_ms"]},
         "rooflines_secondary": secondary,
         "cpu_baseline": cpu,
+        "c4": large,
         "e2e": e2e,
         "e2e_with_ordering": e2e_full,
         "clocks": clk,

@@ -50,6 +50,7 @@ class Options:
     s_max: float = 100.0
     fixed_var_eps: float = 1e-8
     scaling: bool = True
+    verbose: bool = False
 
 
 @dataclass
@@ -280,6 +281,9 @@ def solve(om: M.OModel, lower, upper, start, opts: Options | None = None,
         dphi = float(gpx @ steps.x + (gps @ steps.s if m else 0.0))
 
         alpha, ok, ftype = a_max, False, False
+        if getattr(opts, "verbose", False):
+            print(f"  oracle newton: dw {dw:.3e} ir {rounds} a_max {a_max:.3e} a_z {a_z:.3e} dphi {dphi:.6e}"
+                  f" th_cur {th_cur:.6e} ph_cur {ph_cur:.10e}")
         while alpha >= opts.alpha_min:
             xt, stt = x + alpha * steps.x, s + alpha * steps.s
             try:

@@ -585,6 +585,9 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             return finish(REGULARIZATION_EXHAUSTED, str(exc))
         timer.stop("linear", t0)
         state["reg"] = (ws.delta_w, ws.delta_c)
+        if opts.log_level >= 3:
+            print(f"  newton: delta_w {delta_w:.3e} ir rounds {ir.rounds} "
+                  f"residual {ir.initial_residual:.3e} -> {ir.final_residual:.3e} scale {ir.scale:.3e}")
         report.refinement_relative_residual = ir.relative_residual
         # ---- fraction to the boundary and dphi (ipm.py:455-476)
         tau = max(opts.tau_min, 1.0 - mu)
@@ -616,6 +619,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
                                            L.ptr(P.st), L.ptr(P.scal[54:59]), stream))
             P.flags[0:1].copy_(ev_flags)
             tv, adf, _ = P.read(49, 59)
+            if opts.log_level >= 3:
+                print(f"  trial alpha {alpha:.3e} adf {adf} merit {list(map(float, tv))}")
             if first:
                 first = False
                 alpha = min(float(tv[1]), float(tv[2]))

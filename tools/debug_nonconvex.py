@@ -12,10 +12,10 @@ from test_gpu_ipm import nonconvex_model  # noqa: E402
 
 m = nonconvex_model()
 om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
-for tol in (1e-4, 1e-8):
-    r = solve(m, SolverOptions(tol=tol))
-    o = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol))
-    print("tol", tol, r.status, r.iterations, o.status, o.iterations)
+for tol in [float(t) for t in (sys.argv[1:] or ["1e-4", "1e-8"])]:
+    r = solve(m, SolverOptions(tol=tol, log_level=3))
+    o = OI.solve(om, m.lower, m.upper, m.start, OI.Options(tol=tol, verbose=True))
+    print("tol", tol, r.status, r.iterations, r.message, o.status, o.iterations)
     for a, b in zip(r.trace, o.trace):
         print(" ours", ["%.10g" % v for v in a])
         print(" orac", ["%.10g" % v for v in b])
