@@ -29,7 +29,8 @@ def dense(n, out):
     b = torch.ones(n, dtype=torch.float64, device="cuda")
     for _ in range(3):
         tr, pt = sparse.trace_factor_solve(sym, kv, b)
-    np.savez_compressed(out, trace=tr, panels=pt, **sparse.front_plan(sym))
+    np.savez_compressed(out, trace=tr, panels=pt, probes=getattr(sparse.trace_factor_solve, "last_probes", None),
+                        **sparse.front_plan(sym))
     print("saved", out)
 
 
@@ -44,7 +45,8 @@ def main(wl="C3", out="gpurun_out/trace.npz"):
     for _ in range(2):
         tr, pt = sparse.trace_factor_solve(be.symbolic, be.kvals, b)
     fp = sparse.front_plan(be.symbolic)
-    np.savez_compressed(out, trace=tr, panels=pt, **fp)
+    np.savez_compressed(out, trace=tr, panels=pt, probes=getattr(sparse.trace_factor_solve, "last_probes", None),
+                        **fp)
     print("saved", out, tr.shape)
 
 
