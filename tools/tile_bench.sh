@@ -1,7 +1,8 @@
 #!/bin/bash
-# build + run the PANEL microbenchmark (GPU box)
+# build + run the solve-block microbenchmark (GPU box); tools/tile_bench.cu
+# belongs to the tile-DAG experiment (branch dag-experiment)
 set -e
 cd "$(dirname "$0")/.."
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Iinclude -Ipaper_2307_16830_b200/csrc \
-  tools/tile_bench.cu -o /tmp/tile_bench -Lpaper_2307_16830_b200/_lib -lgridopf -Xlinker -rpath=$(pwd)/paper_2307_16830_b200/_lib
-for m in dd rand; do echo $m; timeout 60 /tmp/tile_bench $m; done
+  tools/fwd_bench.cu -o /tmp/fwd_bench -Lpaper_2307_16830_b200/_lib -lgridopf -Xlinker -rpath=$(pwd)/paper_2307_16830_b200/_lib
+timeout 30 /tmp/fwd_bench
