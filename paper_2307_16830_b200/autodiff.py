@@ -46,12 +46,14 @@ class DeviceEvaluator:
         self.flags = torch.zeros(1, dtype=torch.int32, device=self.contrib.device)
 
     def launch(self, x, what, y=None, obj_weight=1.0, con_scale=None, obj_scale=1.0,
-               f=None, c=None, grad=None, jac=None, hess=None):
-        """Enqueue one evaluation; outputs are caller-provided CUDA tensors."""
+               f=None, c=None, grad=None, jac=None, hess=None, flags=None):
+        """Enqueue one evaluation; outputs are caller-provided CUDA tensors.
+        `flags` (an int32 CUDA tensor) receives the non-finite bits instead of
+        the evaluator's own word (the solver's scalar mailbox)."""
         L.check(L.lib().gn_ad_eval(
             self.handle, L.ptr(x), L.ptr(y), float(obj_weight), L.ptr(con_scale), float(obj_scale),
             L.ptr(f), L.ptr(c), L.ptr(grad), L.ptr(jac), L.ptr(hess), what, L.ptr(self.contrib),
-            L.ptr(self.flags), D.stream_ptr()))
+            L.ptr(self.flags if flags is None else flags), D.stream_ptr()))
 
     def raise_on_flags(self, flags_value: int, order=(F, C, GRAD, JAC, HESS)):
         for bit in order:

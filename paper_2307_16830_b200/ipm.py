@@ -161,23 +161,23 @@ def _mu_candidates(mu, mu_min, opts, k):
 
 
 class _Timer:
-    """CUDA-event phase timing (replaces the reference's perf_counter splits)."""
+    """Host perf_counter phase splits, as the reference keeps them
+    (ipm.py:381-391, 431-453).  CUDA events here cost ~5-10 us of Python per
+    record on the solver's critical path (the GPU waits on the host there);
+    device-side kernel times come from profiling.span / bench.py instead."""
 
     def __init__(self):
-        self.spans = {"ad": [], "linear": []}
+        self.spans = {"ad": 0.0, "linear": 0.0}
 
-    def start(self):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        return e
+    @staticmethod
+    def start():
+        return time.perf_counter()
 
-    def stop(self, name, ev0):
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        self.spans[name].append((ev0, e))
+    def stop(self, name, t0):
+        self.spans[name] += time.perf_counter() - t0
 
     def totals(self):
-        return {k: sum(a.elapsed_time(b) for a, b in v) / 1e3 for k, v in self.spans.items()}
+        return dict(self.spans)
 
 
 def _prepared_inputs(model, opts, ranges) -> dict:
@@ -278,11 +278,18 @@ class _DeviceSolve:
         self.grad, self.c = D.empty(n), D.empty(max(1, m))
         self.dual_x, self.dual_s, self.primal = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
         self.xt, self.st, self.ct = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
-        # scalar mailbox: [0:48) prep | 48 f | 49 f_trial | 50.. misc
-        self.scal = D.zeros(96)
-        self.host = torch.zeros(96, dtype=torch.float64, pin_memory=True)
-        self.host_flags = torch.zeros(2, dtype=torch.int32, pin_memory=True)
-        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)   # [AD flags, IPM flags]
+        # scalar mailbox: [0:48) prep | 48 f | 49 f_trial | 50.. misc, then the
+        # two int32 flag words [AD flags, IPM flags] in the last double, so one
+        # copy brings scalars and flags back; the AD kernels write their flags
+        # into it directly
+        self.mail = D.zeros(97)
+        self.scal = self.mail[:96]
+        self.flags = self.mail[96:].view(torch.int32)
+        self.flag_ad = self.flags[0:1]
+        self.host_mail = torch.zeros(97, dtype=torch.float64, pin_memory=True)
+        self.host = self.host_mail[:96]
+        self.host_flags = self.host_mail[96:].view(torch.int32)
+        self.stream = torch.cuda.current_stream()
 
     def vecs(self, ws) -> L.IpmVecs:
         return L.IpmVecs(*(t.data_ptr() for t in (
@@ -291,25 +298,27 @@ class _DeviceSolve:
             self.c, ws.a_vals, self.dual_x, self.dual_s, self.primal)))
 
     def read_async(self, lo, hi):
-        """Start copying scal[lo:hi] and the flag words; returns the event to wait on."""
-        D.TRANSFER["d2h"] += 8 * (hi - lo) + 8
-        self.host[lo:hi].copy_(self.scal[lo:hi], non_blocking=True)
-        self.host_flags.copy_(self.flags, non_blocking=True)
+        """Start copying scal[lo:hi] and the flag words (one copy); returns
+        the event to wait on."""
+        D.TRANSFER["d2h"] += 8 * (97 - lo)
+        self.host_mail[lo:].copy_(self.mail[lo:], non_blocking=True)
         ev = torch.cuda.Event()
-        ev.record()
+        ev.record(self.stream)
         return ev
 
     def read_wait(self, ev, lo, hi):
         ev.synchronize()
-        return self.host[lo:hi].numpy(), int(self.host_flags[0]), int(self.host_flags[1])
+        f = self.host_flags.tolist()
+        return self.host[lo:hi].numpy(), f[0], f[1]
 
     def read(self, lo, hi):
-        """Copy scal[lo:hi] and both flag words to the host (one stream sync)."""
-        D.TRANSFER["d2h"] += 8 * (hi - lo) + 8
-        self.host[lo:hi].copy_(self.scal[lo:hi], non_blocking=True)
-        self.host_flags.copy_(self.flags, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        return self.host[lo:hi].numpy(), int(self.host_flags[0]), int(self.host_flags[1])
+        """Copy scal[lo:hi] and both flag words to the host (one copy, one
+        stream sync)."""
+        D.TRANSFER["d2h"] += 8 * (97 - lo)
+        self.host_mail[lo:].copy_(self.mail[lo:], non_blocking=True)
+        self.stream.synchronize()
+        f = self.host_flags.tolist()
+        return self.host[lo:hi].numpy(), f[0], f[1]
 
 
 def _plan_lookup(model, ordering):
@@ -384,6 +393,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     backend.n_factorizations = 0
     # the workspace reads the solver's duals in place (no copies per iteration)
     ws.zxl, ws.zxu, ws.zsl, ws.zsu = P.zxl, P.zxu, P.zsl, P.zsu
+    ws.__dict__["_stream"] = P.stream
     ws.delta_w = ws.delta_c = 0.0
     reg = RegState()
     V = P.vecs(ws)
@@ -393,7 +403,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     flagp = L.ptr(P.flags)
 
     def finish(status, message=""):
-        torch.cuda.current_stream().synchronize()
+        P.stream.synchronize()
         total = time.perf_counter() - t_start
         report.status = status
         report.message = message
@@ -402,15 +412,14 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         report.x = D.to_host(P.x)
         try:
             # unscaled objective and bound violation of g(x) (ipm.py:350-357)
-            ev.flags.zero_()
-            ev.launch(P.x, F | C, f=P.scal[62:63], c=P.ct)
+            P.flag_ad.zero_()
+            ev.launch(P.x, F | C, f=P.scal[62:63], c=P.ct, flags=P.flag_ad)
             if m:
                 g = P.ct[:m]
                 zero = torch.zeros_like(g)
                 viol = torch.maximum(torch.maximum(P.rlo_d - g, zero),
                                      torch.maximum(g - P.rhi_d, zero))
                 P.scal[63] = viol.max()
-            P.flags[0:1].copy_(ev.flags)
             fin, adf, _ = P.read(62, 64)
             # ipm.py:352-355: a non-finite objective leaves both NaN; a
             # non-finite g(x) keeps the objective and leaves the violation NaN
@@ -446,9 +455,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     # initial slacks from g(x0) (ipm.py:371-380), on the device; one read
     # returns obj_scale, theta0 and the flags of both evaluations at x0
     P.flags.zero_()
-    ev.flags.zero_()
     t0 = timer.start()
-    ev.launch(P.x, C, con_scale=P.con_scale, c=P.c)
+    ev.launch(P.x, C, con_scale=P.con_scale, c=P.c, flags=P.flag_ad)
     timer.stop("ad", t0)
     if m:
         tol_r, push = P.tol_r, opts.bound_push
@@ -461,7 +469,6 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         P.s.copy_(s0)
         P.scal[60] = (g0 - s0).abs().sum()
     P.scal[61] = P.obj_scale_d
-    P.flags[0:1].copy_(ev.flags)
     P.flags[1:2].copy_(P.flags0)
     sc0, adf0, adf_x0 = P.read(60, 62)
     if adf_x0:
@@ -484,7 +491,6 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
     theta_max = 1e4 * max(1.0, theta0)
     f_ptr = L.ptr(P.scal[48:49])
     ft_ptr = L.ptr(P.scal[49:50])
-    ev_flags = ev.flags
 
     pv_buf = PVec.empty(n, m)
 
@@ -497,14 +503,13 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         with span("ad_full"):
             ev.launch(P.x, F | C | GRAD | JAC | HESS | RESET, y=P.y, obj_weight=P.obj_scale,
                       con_scale=P.con_scale, obj_scale=P.obj_scale, f=P.scal[48:49], c=P.c,
-                      grad=P.grad, jac=ws.a_vals, hess=ws.w_vals)
+                      grad=P.grad, jac=ws.a_vals, hess=ws.w_vals, flags=P.flag_ad)
         timer.stop("ad", t0)
         cands = _mu_candidates(mu, mu_min, opts, L.IPM_MAX_MU)
         mus = (ctypes.c_double * len(cands))(*cands)
         with span("prep"):
             L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal),
                                     stream))
-        P.flags[0:1].copy_(ev_flags)
         return P.read_async(0, 49), cands
 
     pending = launch_eval_prep(state["mu"]) if opts.max_iter > 0 else None
@@ -571,14 +576,14 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             # pivot flag; it comes back with the first refinement read, and
             # only a failure falls back to the regularisation schedule of
             # solve_with_regularization (kkt.py:424-447)
-            dx, ds, dy = backend.solve_pvec(pv)
+            dx, ds, dy = backend.solve_pvec(pv, "main")
             delta_w = 0.0
-            steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
+            steps = assemble_steps(ws, pv, dx, ds, dy, check=False, slot="main")
             try:
                 ir = iterative_refinement(ws, backend, steps, pv, check_factor=backend.fws.fail)
             except FactorizationFailed:
-                (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg)
-                steps = assemble_steps(ws, pv, dx, ds, dy, check=False)
+                (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg, "main")
+                steps = assemble_steps(ws, pv, dx, ds, dy, check=False, slot="main")
                 ir = iterative_refinement(ws, backend, steps, pv)
         except RegularizationExhausted as exc:
             timer.stop("linear", t0)
@@ -613,11 +618,10 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             t0 = timer.start()
             with span("ad_trial"):
                 ev.launch(P.xt, F | C | RESET, con_scale=P.con_scale, obj_scale=P.obj_scale,
-                          f=P.scal[49:50], c=P.ct)
+                          f=P.scal[49:50], c=P.ct, flags=P.flag_ad)
             timer.stop("ad", t0)
             L.check(lib.gn_ipm_trial_merit(ws.handle, ctypes.byref(V), L.ptr(P.ct), L.ptr(P.xt),
                                            L.ptr(P.st), L.ptr(P.scal[54:59]), stream))
-            P.flags[0:1].copy_(ev_flags)
             tv, adf, _ = P.read(49, 59)
             if opts.log_level >= 3:
                 print(f"  trial alpha {alpha:.3e} adf {adf} merit {list(map(float, tv))}")
@@ -671,6 +675,6 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             print(f"iter {state['it']:4d} obj {fval / P.obj_scale: .8e} inf_pr {primal_max:.2e} "
                   f"inf_du {dual_max:.2e} mu {mu:.1e} alpha {alpha:.2e} dw {delta_w:.1e}")
         report.residual_scaled = e_0
-    torch.cuda.current_stream().synchronize()
+    P.stream.synchronize()
     check_ipm_flags(int(P.flags[1].item()))
     return finish(MAX_ITER)

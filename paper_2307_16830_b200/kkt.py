@@ -357,9 +357,25 @@ class KKTWorkspace:
         qx, qs, qy, _ = self._condense(pv)
         return qx, qs, qy
 
-    def _condense(self, pv):
-        qx, rhs = D.empty(self.n), D.empty(self.n)
-        qs, qy = D.empty(self.m), D.empty(self.m)
+    def _buf(self, key, n):
+        """A persistent device buffer per (role, slot): the solver's hot path
+        allocates nothing per call.  The IPM's Newton step ("main") and a
+        refinement correction ("corr") use different slots, so a correction
+        never overwrites the step it refines."""
+        bufs = self.__dict__.setdefault("_bufs", {})
+        t = bufs.get(key)
+        if t is None or t.numel() != n:
+            t = D.empty(n)
+            bufs[key] = t
+        return t
+
+    def _condense(self, pv, slot=None):
+        if slot is None:
+            qx, rhs = D.empty(self.n), D.empty(self.n)
+            qs, qy = D.empty(self.m), D.empty(self.m)
+        else:
+            qx, rhs = self._buf(("qx", slot), self.n), self._buf(("rhs", slot), self.n)
+            qs, qy = self._buf(("qs", slot), self.m), self._buf(("qy", slot), self.m)
         st, pc = self.state(), pv.c_struct()
         L.check(L.lib().gn_kkt_condense_rhs(self.handle, ctypes.byref(st), ctypes.byref(pc),
                                             L.ptr(qx), L.ptr(qs), L.ptr(qy), L.ptr(rhs),
@@ -370,16 +386,23 @@ class KKTWorkspace:
         z_n, z_m = D.zeros(self.n), D.zeros(self.m)
         return self._condense(PVec(qx, qs, qy, z_n, z_n, z_m, z_m))[3]
 
-    def recover_slack_dual(self, dx, qx, qs, qy):
-        ds, dy = D.empty(self.m), D.empty(self.m)
+    def recover_slack_dual(self, dx, qx, qs, qy, slot=None):
+        if slot is None:
+            ds, dy = D.empty(self.m), D.empty(self.m)
+        else:
+            ds, dy = self._buf(("ds", slot), self.m), self._buf(("dy", slot), self.m)
         st = self.state()
         L.check(L.lib().gn_kkt_recover_slack_dual(self.handle, ctypes.byref(st), L.ptr(D.to_dev(dx)),
                                                   L.ptr(D.to_dev(qs)), L.ptr(D.to_dev(qy)), L.ptr(ds),
                                                   L.ptr(dy), D.stream_ptr()))
         return ds, dy
 
-    def recover_bound_duals(self, dx, ds, pv: PVec, check=True):
-        out = [D.empty(k) for k in (self.n, self.n, self.m, self.m)]
+    def recover_bound_duals(self, dx, ds, pv: PVec, check=True, slot=None):
+        if slot is None:
+            out = [D.empty(k) for k in (self.n, self.n, self.m, self.m)]
+        else:
+            out = [self._buf((f, slot), k) for f, k in zip(("zxl", "zxu", "zsl", "zsu"),
+                                                          (self.n, self.n, self.m, self.m))]
         st, pc = self.state(), pv.c_struct()
         if check:
             self.flags.zero_()
@@ -391,9 +414,17 @@ class KKTWorkspace:
         return tuple(out)
 
     # -- full seven-block system ----------------------------------------------
-    def residual_full(self, st_: Steps, pv: PVec, norm_out=None):
-        """pv - M_full * steps, accumulated in double-double (kkt.py:190-209)."""
-        res = PVec.empty(self.n, self.m)
+    def residual_full(self, st_: Steps, pv: PVec, norm_out=None, reuse=False):
+        """pv - M_full * steps, accumulated in double-double (kkt.py:190-209).
+        reuse: into the workspace's persistent residual (the refinement loop,
+        which consumes each residual before the next one is formed)."""
+        if reuse:
+            res = self.__dict__.get("_res")
+            if res is None:
+                res = PVec.empty(self.n, self.m)
+                self.__dict__["_res"] = res
+        else:
+            res = PVec.empty(self.n, self.m)
         st, sc, pc, rc = self.state(), st_.c_struct(), pv.c_struct(), res.c_struct()
         norm = norm_out if norm_out is not None else self._scal[0:2]
         L.check(L.lib().gn_kkt_residual(self.handle, ctypes.byref(st), ctypes.byref(sc),
@@ -481,19 +512,20 @@ class CondensedBackend:
         ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
         return dx, ds, dy
 
-    def solve_pvec(self, pv: PVec):
-        """Fused condense_pvec + solve3 for the solver's hot path."""
+    def solve_pvec(self, pv: PVec, slot=None):
+        """Fused condense_pvec + solve3 for the solver's hot path (outputs in
+        the workspace's persistent buffers of `slot` when given)."""
         ws = self.ws
         with span("rhs"):
-            qx, qs, qy, rhs = ws._condense(pv)
+            qx, qs, qy, rhs = ws._condense(pv, slot)
         with span("solve"):
-            dx = S.solve_device(self.factor, rhs, D.empty(ws.n))
+            dx = S.solve_device(self.factor, rhs, D.empty(ws.n) if slot is None else ws._buf(("dx", slot), ws.n))
         with span("recover"):
-            ds, dy = ws.recover_slack_dual(dx, qx, qs, qy)
+            ds, dy = ws.recover_slack_dual(dx, qx, qs, qy, slot)
         return dx, ds, dy
 
 
-def solve_with_regularization(ws, backend, pv: PVec, reg: RegState):
+def solve_with_regularization(ws, backend, pv: PVec, reg: RegState, slot=None):
     """Factorize with the inertia-correction schedule, then solve (kkt.py:424-447)."""
     ws.delta_w = 0.0
     ws.delta_c = 0.0
@@ -508,18 +540,25 @@ def solve_with_regularization(ws, backend, pv: PVec, reg: RegState):
                     f"delta_w exceeded {DELTA_W_MAX:g} without positive definiteness")
         reg.delta_w_last = ws.delta_w
     if hasattr(backend, "solve_pvec"):
-        dx, ds, dy = backend.solve_pvec(pv)
+        dx, ds, dy = backend.solve_pvec(pv, slot)
     else:
         qx, qs, qy = ws.condense_pvec(pv)
         dx, ds, dy = backend.solve3(qx, qs, qy)
     return (dx, ds, dy), ws.delta_w
 
 
-def assemble_steps(ws, pv: PVec, dx, ds, dy, check=True) -> Steps:
-    dz = ws.recover_bound_duals(dx, ds, pv, check=check)
+def assemble_steps(ws, pv: PVec, dx, ds, dy, check=True, slot=None) -> Steps:
+    dz = ws.recover_bound_duals(dx, ds, pv, check=check, slot=slot)
+    if slot is not None:   # the slot's Steps object: same buffers, pointer struct kept
+        cache = ws.__dict__.setdefault("_steps", {})
+        st = cache.get(slot)
+        if st is not None and st.x is dx and st.s is ds and st.y is dy and st.zxl is dz[0]:
+            return st
     st = Steps.__new__(Steps)
     st.x, st.s, st.y = D.to_dev(dx), D.to_dev(ds), D.to_dev(dy)
     st.zxl, st.zxu, st.zsl, st.zsu = dz
+    if slot is not None:
+        ws.__dict__["_steps"][slot] = st
     return st
 
 
@@ -542,7 +581,8 @@ def _read4(ws, scal):
         pin = torch.zeros(4, dtype=torch.float64, pin_memory=True)
         object.__setattr__(ws, "_pin4", pin)
     pin.copy_(scal[0:4], non_blocking=True)
-    torch.cuda.current_stream().synchronize()
+    st = ws.__dict__.get("_stream")
+    (st if st is not None else torch.cuda.current_stream()).synchronize()
     return pin.numpy()
 
 
@@ -560,7 +600,7 @@ def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None)
     """
     scal = ws._scal
     ws.matrix_scale_device(scal[2:3])
-    res = ws.residual_full(steps, pv, norm_out=scal[0:2])
+    res = ws.residual_full(steps, pv, norm_out=scal[0:2], reuse=True)
     if check_factor is not None:
         scal[3:4].copy_(check_factor)
     host = _read4(ws, scal)
@@ -570,10 +610,10 @@ def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None)
     target = KAPPA_IR * np.finfo(float).eps * scale
     stats = RefinementStats(initial_residual=rnorm, final_residual=rnorm, scale=scale)
     while stats.final_residual > target and stats.rounds < MAX_IR_ROUNDS:
-        dx, ds, dy = backend.solve_pvec(res)
-        corr = assemble_steps(ws, res, dx, ds, dy, check=False)
+        dx, ds, dy = backend.solve_pvec(res, "corr")
+        corr = assemble_steps(ws, res, dx, ds, dy, check=False, slot="corr")
         _bind(ws.handle, steps, corr, 1.0)
-        res = ws.residual_full(steps, pv, norm_out=scal[0:2])
+        res = ws.residual_full(steps, pv, norm_out=scal[0:2], reuse=True)
         new = float(_read4(ws, scal)[0])
         stats.rounds += 1
         if new >= stats.final_residual:
