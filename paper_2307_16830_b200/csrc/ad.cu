@@ -438,7 +438,7 @@ static void upload_model(Model &M) {
     cta += (b.R + kRecThreads - 1) / kRecThreads;
     for (int t = 0; t < d.T; ++t) tape.push_back(make_int4(b.ops[3 * t], b.ops[3 * t + 1], b.ops[3 * t + 2], 0));
     consts.insert(consts.end(), b.consts.begin(), b.consts.end());
-    GN_REQUIRE(b.consts.size() <= static_cast<size_t>(kMaxTape), "too many constants in a tape");
+
     for (int s : b.first) slots.push_back(s);
     std::vector<int> sw;
     for (int p = 0; p < d.npairs; ++p) slots.push_back(b.pairs[2 * p]);
@@ -513,6 +513,9 @@ static void upload_model(Model &M) {
   } else {
     M.pattern_error = "disabled by GN_AD_INTERPRETER=1";
   }
+  GN_REQUIRE(M.pattern_fn || !M.needs_patterns,
+             "a pattern block's tape or slot count exceeds the device interpreter's limits (64 entries, "
+             "16 slots); it needs the generated pattern kernels (NVRTC), unavailable: " + M.pattern_error);
   M.uploaded = true;
 }
 

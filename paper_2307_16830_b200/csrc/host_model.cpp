@@ -207,8 +207,11 @@ extern "C" int gn_model_create(const gn_block_desc *blocks, int32_t nblocks, int
         h.np = d.n_param_slots;
         h.out = d.out;
         h.R = d.n_records;
-        GN_REQUIRE(d.n_ops <= kMaxTape, "instruction tape longer than the device limit (64)");
-        GN_REQUIRE(h.nv <= kMaxSlots, "more than 16 variable slots per record");
+        // longer tapes / more slots than the interpreter holds run on the
+        // generated pattern kernels only (checked again at upload)
+        GN_REQUIRE(d.n_ops <= kMaxTapeGen, "instruction tape longer than 4096 entries");
+        GN_REQUIRE(h.nv <= kMaxSlotsGen, "more than 256 variable slots per record");
+        if (d.n_ops > kMaxTape || h.nv > kMaxSlots || d.n_consts > kMaxTape) M->needs_patterns = true;
         GN_REQUIRE(d.kind == 0 || d.targets != nullptr || h.R == 0, "constraint block without targets");
         h.var_idx.assign(d.var_idx, d.var_idx + h.R * h.nv);
         h.params.assign(d.params, d.params + h.R * h.np);

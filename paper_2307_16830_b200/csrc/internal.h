@@ -66,8 +66,13 @@ int guarded(F &&f) {
   }
 }
 
-constexpr int kMaxTape = 64;   // device interpreter: tape entries per instruction
-constexpr int kMaxSlots = 16;  // variable slots per record
+constexpr int kMaxTape = 64;   // device INTERPRETER: tape entries per instruction
+constexpr int kMaxSlots = 16;  // device INTERPRETER: variable slots per record
+// the generated pattern kernels (ad_codegen.cpp) keep a tape's values in
+// registers / local memory and have no structural limit; these bound the
+// generated source size only
+constexpr int kMaxTapeGen = 4096;
+constexpr int kMaxSlotsGen = 256;
 
 // ---------------------------------------------------------------- AD plan
 struct DevBlock {                // one pattern block as seen by the device
@@ -114,6 +119,7 @@ struct Model {
   void *d_genblk = nullptr;          // its per-block table (device)
   std::string pattern_error;         // why the interpreter is used, if it is
   bool jac_direct = false;           // every J slot has exactly one contribution
+  bool needs_patterns = false;       // a tape / slot count beyond the interpreter's limits
   int batch_cap = 0;                 // instances the objective scratch holds
   int64_t n_params = 0;              // device parameter layout size (doubles)
   struct Dev {

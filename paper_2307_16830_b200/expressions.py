@@ -30,7 +30,7 @@ BINARY = frozenset((ADD, SUB, MUL, DIV))
 # unary operators whose second derivative is nonzero
 _CURVED_UNARY = frozenset((SIN, COS, LOG, SQRT, EXP))
 
-MAX_TAPE = 64   # device interpreter limit (registers/local memory per record)
+MAX_TAPE = 64   # device interpreter limit; longer tapes run on the generated pattern kernels
 
 
 class Expr:

@@ -391,3 +391,52 @@ def test_generated_pattern_kernels_match_interpreter():
             scale = max(1.0, np.max(np.abs(r)))
             assert np.max(np.abs(a - b)) <= 1e-14 * scale
             assert np.max(np.abs(a - r)) <= 1e-12 * scale
+
+
+@pytest.mark.gpu
+def test_long_tape_runs_on_generated_kernels():
+    """Tapes beyond the interpreter's 64 entries (the reference tape has no
+    cap, expressions.py:147-219) run on the generated pattern kernels and
+    match the oracle; with the interpreter forced, model upload fails loudly
+    instead of truncating."""
+    import os
+
+    from paper_2307_16830_b200 import ModelBuilder
+    from paper_2307_16830_b200.expressions import cos, param, sin, var
+
+    k = 24   # ~150 tape entries: sum_k p_k sin(x0 p_k + x1) cos(x2 - p_k)
+    expr = None
+    for j in range(k):
+        t = param(j) * sin(var(0) * param(j) + var(1)) * cos(var(2) - param(j))
+        expr = t if expr is None else expr + t
+    rng = np.random.default_rng(5)
+    R, n = 40, 6
+    vi = np.stack([rng.choice(n, 3, replace=False) for _ in range(R)])
+    pa = rng.uniform(0.2, 1.5, (R, k))
+
+    def build():
+        b = ModelBuilder()
+        b.add_variables(n, -np.ones(n) * 3, np.ones(n) * 3, np.zeros(n))
+        b.add_objective(expr, vi, pa)
+        b.add_constraints(expr, vi, pa)
+        return b.finalize()
+
+    m = build()
+    assert len(m.pattern_blocks[0].tape.ops) > 64
+    x = rng.uniform(-1, 1, n)
+    yv = rng.standard_normal(m.n_con)
+    om = OM.expand(m.n_var, m.n_con, OM.from_model(m))
+    got = (ad.eval_objective(m, x), ad.eval_constraints(m, x), ad.eval_gradient(m, x),
+           ad.eval_jacobian(m, x), ad.eval_lagrangian_hessian(m, x, yv, 0.7))
+    ref = (OM.objective(om, x), OM.constraints(om, x), OM.gradient(om, x), OM.jacobian(om, x),
+           OM.hessian(om, x, yv, 0.7))
+    for a, r in zip(got, ref):
+        a, r = np.atleast_1d(a), np.atleast_1d(r)
+        assert np.max(np.abs(a - r)) <= 1e-12 * max(1.0, np.max(np.abs(r)))
+    os.environ["GN_AD_INTERPRETER"] = "1"
+    try:
+        m2 = build()
+        with pytest.raises(Exception, match="interpreter"):
+            ad.eval_gradient(m2, x)
+    finally:
+        os.environ.pop("GN_AD_INTERPRETER", None)
