@@ -1,4 +1,5 @@
 // Error reporting and launch/transfer accounting for the C-ABI (gridopf.h).
+#include <malloc.h>
 #include <omp.h>
 
 #include <atomic>
@@ -10,6 +11,20 @@
 #include "internal.h"
 
 namespace gn {
+// Host heap policy.  The symbolic analysis of every solve builds and drops
+// tens of MB of index arrays; with glibc's defaults those large blocks are
+// mmap'd and unmapped per call, so every solve pays a fresh page fault per
+// 4 KiB (about half of the C3 condensation's time).  Serving them from the
+// heap and never trimming it keeps the pages mapped across solves.
+// GN_HOST_HEAP_RETAIN=0 keeps the allocator's defaults.
+__attribute__((constructor)) static void host_heap_policy() {
+  const char *e = std::getenv("GN_HOST_HEAP_RETAIN");
+  if (e && e[0] == '0') return;
+  mallopt(M_MMAP_MAX, 0);                 // no per-allocation mmap
+  mallopt(M_TRIM_THRESHOLD, 1 << 30);     // keep freed heap pages mapped
+  mallopt(M_TOP_PAD, 16 << 20);
+}
+
 static thread_local std::string g_last_error;
 static std::atomic<int64_t> g_launches{0};
 static std::atomic<int64_t> g_h2d{0};

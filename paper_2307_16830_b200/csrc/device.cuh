@@ -37,8 +37,8 @@ void *dev_malloc(size_t bytes);   // cached device allocation (alloc.cu)
 void dev_free(void *p);
 void alloc_trim();               // return cached blocks to the driver
 
-template <class T>
-T *dev_upload(const std::vector<T> &v) {
+template <class T, class A>
+T *dev_upload(const std::vector<T, A> &v) {
   T *p = static_cast<T *>(dev_malloc(sizeof(T) * (v.empty() ? 1 : v.size())));
   const bool tm = timing_on();
   const double t0 = tm ? host_now() : 0.0;

@@ -160,27 +160,40 @@ int64_t Condense::product_segment(int64_t q) const {
   return static_cast<int64_t>(std::upper_bound(seg_poff.begin(), seg_poff.end(), q) - seg_poff.begin()) - 1;
 }
 
+// Condensed pattern K = tril(W + I + A^T A) straight from the factors, one
+// column at a time (a symbolic sparse product, no coordinate list): column c
+// collects its W rows, the diagonal, and for every Jacobian row r holding c
+// the entries of r at or after c.  A second pass over the same column writes
+// the sorted rows, the slot of each W/diagonal/product coordinate and the
+// column's slice of the assembly plan -- the products grouped by K slot in
+// ascending product index (kkt.py:243-283 summation order), which is the
+// order a column visits them: Jacobian rows ascending, then la ascending.
+// Columns are independent, so both passes are parallel over columns.
 static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, const int64_t *hc,
                      int64_t nj, const int64_t *jr, const int64_t *jc) {
   PhaseTimer tm_total("condense.total");
   C.n = n;
   C.nnz_h = nh;
   C.nnz_j = nj;
-  GN_REQUIRE(n < (int64_t(1) << 31), "too many variables for 32-bit indices");
+  GN_REQUIRE(n < (int64_t(1) << 31) && nh < (int64_t(1) << 31) && nj < (int64_t(1) << 31),
+             "too many variables or nonzeros for 32-bit indices");
   int bad = 0;
 #pragma omp parallel for reduction(| : bad)
-  for (int64_t t = 1; t < nj; ++t)
-    bad |= !(jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1]));
-  GN_REQUIRE(!bad, "Jacobian coordinates must be sorted row-major and unique");
+  for (int64_t t = 0; t < nj; ++t)
+    bad |= !(jc[t] >= 0 && jc[t] < n &&
+             (t == 0 || jr[t] > jr[t - 1] || (jr[t] == jr[t - 1] && jc[t] > jc[t - 1])));
+  GN_REQUIRE(!bad, "Jacobian coordinates must be sorted row-major, unique and in range");
 #pragma omp parallel for reduction(| : bad)
   for (int64_t t = 0; t < nh; ++t) bad |= !(hc[t] <= hr[t] && hr[t] >= 0 && hr[t] < n && hc[t] >= 0);
   GN_REQUIRE(!bad, "Hessian entry out of range or above the diagonal");
   // Jacobian row segments and their product offsets (np.tril_indices order)
   C.seg.clear();
   C.seg_row.clear();
+  std::vector<int32_t> pseg(nj);
   for (int64_t st = 0; st < nj;) {
     int64_t en = st;
     while (en < nj && jr[en] == jr[st]) ++en;
+    for (int64_t e = st; e < en; ++e) pseg[e] = static_cast<int32_t>(C.seg.size());
     C.seg.push_back(st);
     C.seg_row.push_back(jr[st]);
     st = en;
@@ -197,84 +210,115 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
   C.np = np;
   GN_REQUIRE(np < (int64_t(1) << 31), "too many A^T A products for 32-bit offsets");
   PhaseTimer tm_all("condense");
-  const int64_t base = nh + n;
-  std::vector<int32_t> rows(base + np), cols(base + np), pseg(np);
-#pragma omp parallel for
-  for (int64_t t = 0; t < nh; ++t) {
-    rows[t] = static_cast<int32_t>(hr[t]);
-    cols[t] = static_cast<int32_t>(hc[t]);
-  }
-#pragma omp parallel for
-  for (int64_t i = 0; i < n; ++i) rows[nh + i] = cols[nh + i] = static_cast<int32_t>(i);
-#pragma omp parallel for schedule(dynamic, 256)
-  for (int64_t g = 0; g < nseg; ++g) {
-    const int64_t st = C.seg[g], en = C.seg[g + 1];
-    int64_t q = C.seg_poff[g];
-    for (int64_t la = 0; la < en - st; ++la)
-      for (int64_t lb = 0; lb <= la; ++lb, ++q) {
-        rows[base + q] = static_cast<int32_t>(jc[st + la]);
-        cols[base + q] = static_cast<int32_t>(jc[st + lb]);
-        pseg[q] = static_cast<int32_t>(g);
-      }
-  }
-  std::vector<int64_t> bptr;
-  std::vector<int32_t> bucket;
-  {
-    PhaseTimer tm("condense.csc_from_coords");
-    csc_from_coords(n, rows, cols, C.indptr, C.indices, C.slot, &bucket, &bptr);
-  }
-  // the assembly plan is built on first use (gn_kkt_create, usually on the
-  // launching thread while the analysis worker runs the symbolic factor)
-  C.plan_bucket = std::move(bucket);
-  C.plan_bptr = std::move(bptr);
-  C.plan_pseg = std::move(pseg);
-}
-
-// assembly plan: the A^T A products grouped by K slot, ascending product
-// index inside a slot (the summation order of kkt.py:243-283).  The column
-// buckets already hold every coordinate of a column in input order, and a
-// slot belongs to one column, so columns are processed independently.
-void Condense::ensure_assembly_plan() {
-  std::lock_guard<std::mutex> g(plan_mu);
-  if (plan_built) return;
-  PhaseTimer tm_plan("condense.assembly_plan");
-  const int64_t nk = indptr[n], base = nnz_h + n;
-  const std::vector<int32_t> &bucket = plan_bucket, &pseg = plan_pseg;
-  const std::vector<int64_t> &bptr = plan_bptr;
-  k_ptr.assign(nk + 1, 0);
-  k_row.resize(np);
-  k_s1.resize(np);
-  k_s2.resize(np);
-#pragma omp parallel for schedule(dynamic, 512)
-  for (int64_t c = 0; c < n; ++c)
-    for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q)
-      if (bucket[q] >= base) k_ptr[slot[bucket[q]] + 1]++;
-  for (int64_t s = 0; s < nk; ++s) k_ptr[s + 1] += k_ptr[s];
+  // Jacobian entries by column (ascending entry, hence ascending row) and
+  // W entries by column (input order)
+  PhaseTimer tm_b("condense.buckets");
+  std::vector<int64_t> aptr, hptr;
+  std::vector<int32_t> alist(nj), hlist(nh);
+  par_bucket(n, nj, [&](int64_t p) { return jc[p]; },
+             [&](int64_t p, int64_t d) { alist[d] = static_cast<int32_t>(p); }, aptr);
+  par_bucket(n, nh, [&](int64_t t) { return hc[t]; },
+             [&](int64_t t, int64_t d) { hlist[d] = static_cast<int32_t>(t); }, hptr);
+  tm_b.~PhaseTimer();
+  new (&tm_b) PhaseTimer("condense.pass1");
+  // pass 1: unique rows and products per column
+  std::vector<int64_t> ucount(n), pcount(n);
 #pragma omp parallel
   {
+    std::vector<int32_t> mark(n, -1);
+#pragma omp for schedule(dynamic, 512)
+    for (int64_t c = 0; c < n; ++c) {
+      int64_t u = 1, prods = 0;
+      mark[c] = static_cast<int32_t>(c);
+      for (int64_t k = hptr[c]; k < hptr[c + 1]; ++k) {
+        const int64_t r = hr[hlist[k]];
+        if (mark[r] != c) mark[r] = static_cast<int32_t>(c), ++u;
+      }
+      for (int64_t k = aptr[c]; k < aptr[c + 1]; ++k) {
+        const int64_t p = alist[k], en = C.seg[pseg[p] + 1];
+        prods += en - p;
+        for (int64_t e = p; e < en; ++e)
+          if (mark[jc[e]] != c) mark[jc[e]] = static_cast<int32_t>(c), ++u;
+      }
+      ucount[c] = u;
+      pcount[c] = prods;
+    }
+  }
+  tm_b.~PhaseTimer();
+  new (&tm_b) PhaseTimer("condense.alloc");
+  C.indptr.assign(n + 1, 0);
+  std::vector<int64_t> pptr(n + 1, 0);
+  for (int64_t c = 0; c < n; ++c) {
+    C.indptr[c + 1] = C.indptr[c] + ucount[c];
+    pptr[c + 1] = pptr[c] + pcount[c];
+  }
+  const int64_t nk = C.indptr[n], base = nh + n;
+  C.indices.resize(nk);
+  C.slot.resize(base + np);
+  C.k_ptr.resize(nk + 1);
+  C.k_row.resize(np);
+  C.k_s1.resize(np);
+  C.k_s2.resize(np);
+  tm_b.~PhaseTimer();
+  new (&tm_b) PhaseTimer("condense.pass2");
+  // pass 2: sorted rows, slots, assembly plan
+#pragma omp parallel
+  {
+    std::vector<int32_t> mark(n, -1);
+    std::vector<int64_t> pos(n, 0);
     std::vector<int32_t> fill;
 #pragma omp for schedule(dynamic, 512)
     for (int64_t c = 0; c < n; ++c) {
-      const int64_t s0 = indptr[c];
-      fill.assign(k_ptr.begin() + s0, k_ptr.begin() + indptr[c + 1]);
-      for (int64_t q = bptr[c]; q < bptr[c + 1]; ++q) {
-        const int64_t t = bucket[q];
-        if (t < base) continue;
-        const int64_t p = t - base;
-        int64_t row, s1, s2;
-        product(p, pseg[p], row, s1, s2);
-        const int32_t d = fill[slot[t] - s0]++;
-        k_row[d] = static_cast<int32_t>(row);
-        k_s1[d] = static_cast<int32_t>(s1);
-        k_s2[d] = static_cast<int32_t>(s2);
+      const int64_t s0 = C.indptr[c];
+      int64_t u = s0;
+      mark[c] = static_cast<int32_t>(c);
+      C.indices[u++] = c;
+      for (int64_t k = hptr[c]; k < hptr[c + 1]; ++k) {
+        const int64_t r = hr[hlist[k]];
+        if (mark[r] != c) mark[r] = static_cast<int32_t>(c), C.indices[u++] = r;
+      }
+      for (int64_t k = aptr[c]; k < aptr[c + 1]; ++k) {
+        const int64_t p = alist[k], en = C.seg[pseg[p] + 1];
+        for (int64_t e = p; e < en; ++e)
+          if (mark[jc[e]] != c) mark[jc[e]] = static_cast<int32_t>(c), C.indices[u++] = jc[e];
+      }
+      std::sort(C.indices.begin() + s0, C.indices.begin() + u);
+      for (int64_t t = s0; t < u; ++t) pos[C.indices[t]] = t;
+      for (int64_t k = hptr[c]; k < hptr[c + 1]; ++k) C.slot[hlist[k]] = pos[hr[hlist[k]]];
+      C.slot[nh + c] = pos[c];
+      // products of the column per slot, then their plan entries
+      fill.assign(u - s0, 0);
+      for (int64_t k = aptr[c]; k < aptr[c + 1]; ++k) {
+        const int64_t p = alist[k], en = C.seg[pseg[p] + 1];
+        for (int64_t e = p; e < en; ++e) fill[pos[jc[e]] - s0]++;
+      }
+      int32_t run = static_cast<int32_t>(pptr[c]);
+      for (int64_t t = s0; t < u; ++t) {
+        const int32_t h = fill[t - s0];
+        C.k_ptr[t] = run;
+        fill[t - s0] = run;
+        run += h;
+      }
+      for (int64_t k = aptr[c]; k < aptr[c + 1]; ++k) {
+        const int64_t p = alist[k], g = pseg[p], st = C.seg[g], en = C.seg[g + 1];
+        const int64_t lb = p - st, qb = C.seg_poff[g] + lb;
+        for (int64_t e = p; e < en; ++e) {
+          const int64_t la = e - st, s = pos[jc[e]];
+          C.slot[base + qb + la * (la + 1) / 2] = s;
+          const int32_t d = fill[s - s0]++;
+          C.k_row[d] = static_cast<int32_t>(C.seg_row[g]);
+          C.k_s1[d] = static_cast<int32_t>(e);
+          C.k_s2[d] = static_cast<int32_t>(p);
+        }
       }
     }
   }
-  std::vector<int32_t>().swap(plan_bucket);
-  std::vector<int64_t>().swap(plan_bptr);
-  std::vector<int32_t>().swap(plan_pseg);
-  plan_built = true;
+  C.k_ptr[nk] = static_cast<int32_t>(np);
+  C.plan_built = true;
 }
+
+// the plan is built with the pattern (kept for callers of the old split)
+void Condense::ensure_assembly_plan() {}
 
 // ------------------------------------------------------------ ordering
 // Explicit elimination graph exactly as the reference builds it: eliminating
@@ -444,7 +488,7 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
       }
     }
     for (int64_t k = 0; k < n; ++k) S.row_ptr[k + 1] = S.row_ptr[k] + rc[k];
-    S.row_cols.assign(S.row_ptr[n], 0);
+    S.row_cols.resize(S.row_ptr[n]);   // etree-reach order; sorted on export
 #pragma omp parallel
     {
       std::vector<int64_t> mark(n, -1);
@@ -457,7 +501,6 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
             mark[i] = k;
             S.row_cols[o++] = i;
           }
-        std::sort(S.row_cols.begin() + S.row_ptr[k], S.row_cols.begin() + o);
       }
     }
   }
@@ -774,8 +817,8 @@ extern "C" int gn_condense_info(const gn_condense *C, int64_t *nnz_k, int64_t *n
   });
 }
 
-template <class T>
-static void copy_out(T *dst, const std::vector<T> &v) {
+template <class T, class A>
+static void copy_out(T *dst, const std::vector<T, A> &v) {
   if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(T) * v.size());
 }
 
@@ -896,7 +939,12 @@ extern "C" int gn_symbolic_export(const gn_symbolic *S, int64_t *parent, int64_t
     copy_out(a_rowcol, S->a_rowcol);
     copy_out(a_srcslot, S->a_srcslot);
     copy_out(row_ptr, S->row_ptr);
-    copy_out(row_cols, S->row_cols);
+    if (row_cols) {   // the reference's sorted row patterns
+      copy_out(row_cols, S->row_cols);
+      const int64_t n = S->n;
+#pragma omp parallel for schedule(dynamic, 1024)
+      for (int64_t k = 0; k < n; ++k) std::sort(row_cols + S->row_ptr[k], row_cols + S->row_ptr[k + 1]);
+    }
     copy_out(l_colptr, S->l_colptr);
     if (l_rowidx) {
       const_cast<Symbolic *>(static_cast<const Symbolic *>(S))->ensure_l_csc();

@@ -6,9 +6,36 @@
 #include <stdexcept>
 #include <string>
 #include <mutex>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "../../include/gridopf.h"
+
+namespace gn {
+// std::allocator that default-initialises: resize() of a uvec leaves
+// trivial elements unwritten (the host analysis fills its big index arrays
+// itself; zero-filling them first cost a serial memset per solve)
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U> &) noexcept {}
+  template <class U, class... A>
+  void construct(U *p, A &&...a) {
+    if constexpr (sizeof...(A) == 0)
+      ::new (static_cast<void *>(p)) U;
+    else
+      ::new (static_cast<void *>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using uvec = std::vector<T, NoInitAlloc<T>>;
+}  // namespace gn
 
 namespace gn {
 
@@ -148,18 +175,16 @@ struct Model {
 // --------------------------------------------------------- condensation
 struct Condense {
   int64_t n = 0, nnz_h = 0, nnz_j = 0, np = 0;
-  std::vector<int64_t> indptr, indices;
+  std::vector<int64_t> indptr;
+  uvec<int64_t> indices;
   // K slot of every coordinate, in input order: the nnz_h W entries
   // (w_map), the n diagonal entries (diag_map), the np A^T A products
   // (ata_map) -- the reference's three maps as slices of one array
-  std::vector<int64_t> slot;
+  uvec<int64_t> slot;
   // Jacobian row segments: start, product offset (np.tril_indices order),
   // constraint row; one trailing entry
   std::vector<int64_t> seg, seg_poff, seg_row;
-  std::vector<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
-  // inputs of the assembly plan until it is built (ensure_assembly_plan)
-  std::vector<int32_t> plan_bucket, plan_pseg;
-  std::vector<int64_t> plan_bptr;
+  uvec<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
   bool plan_built = false;
   std::mutex plan_mu;
   void ensure_assembly_plan();
@@ -188,8 +213,8 @@ struct alignas(16) FrontMeta {
 
 struct Symbolic {
   int64_t n = 0, nnz_a = 0, nnz_l = 0;
-  std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, row_cols,
-      l_colptr;
+  std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, l_colptr;
+  uvec<int64_t> row_cols;   // row patterns of L, each row in etree-reach order
   // the reference L row indices (CSC) and the L -> front map are only needed
   // for exports: built on first use (ensure_l_csc / ensure_l_export)
   std::vector<int64_t> l_rowidx;
