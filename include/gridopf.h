@@ -339,6 +339,24 @@ int gn_ipm_trial_merit(gn_kkt *k, const gn_ipm_vecs *v, const double *ct, const 
 int gn_ipm_accept(gn_kkt *k, const gn_ipm_vecs *v, const gn_vec7 *steps, double alpha,
                   double alpha_z, double mu, double kappa_sigma, int32_t *flags, void *stream);
 
+/* problem setup of one solve (replaces the _Problem constructor's scaling,
+ * relax_equalities and the start/dual initialisation, ipm.py:112-123,
+ * 179-193, 360-369): from g0 = grad f(x0) and j0 = J(x0) (row-major COO rows
+ * jac_rows on the device) obj_scale / con_scale (when `scaling`), the relaxed
+ * slack bounds sl/su of the scaled ranges [rlo, rhi], x = x0, s = y = 0 and
+ * the unit bound duals of the finite bounds.  scratch: m + 1 uint64. */
+int gn_ipm_setup(int64_t n, int64_t m, int64_t nj, const double *g0, const double *j0,
+                 const int64_t *jac_rows, const double *x0, const double *xl, const double *xu,
+                 const double *rlo, const double *rhi, int32_t scaling, double tol_r, uint64_t *scratch,
+                 double *x, double *s, double *y, double *zxl, double *zxu, double *zsl, double *zsu,
+                 double *con_scale, double *sl, double *su, double *obj_scale, void *stream);
+/* initial slacks (ipm.py:371-380): s = clip(g, sl + push_tol, su - push_tol)
+ * (midpoint of [sl, su] where that interval is empty) and theta = sum |g - s|.
+ * red_partials: GN_RED_PARTIALS doubles; red_counter: one zeroed uint32 (left
+ * zeroed). */
+#define GN_RED_PARTIALS (296 * 40)
+int gn_ipm_init_slacks(int64_t m, const double *g, const double *sl, const double *su, double push_tol,
+                       double *s, double *theta, double *red_partials, uint32_t *red_counter, void *stream);
 
 /* ---- batched entry points (K12; layout and bp/scal conventions above).
  * Each replaces B back-to-back calls of its single-instance counterpart on

@@ -49,6 +49,7 @@ class IpmVecs(ctypes.Structure):
 IPM_MAX_MU = 16
 PREP_S = 24
 PREP_DOUBLES = 48
+GN_RED_PARTIALS = 296 * 40   # gridopf.h: reduction scratch of gn_ipm_init_slacks
 
 
 class GridOpfError(RuntimeError):
@@ -110,6 +111,9 @@ _SIGS = {
     "gn_ipm_trial_merit": (c_i32, [P, P, P, P, P, P, P]),
     "gn_ipm_trial_point_at": (c_i32, [P, P, P, P, P, P, P]),
     "gn_ipm_accept": (c_i32, [P, P, P, c_dbl, c_dbl, c_dbl, c_dbl, P, P]),
+    "gn_ipm_setup": (c_i32, [c_i64, c_i64, c_i64, P, P, P, P, P, P, P, P, c_i32, c_dbl, P, P, P, P, P, P, P,
+                             P, P, P, P, P, P]),
+    "gn_ipm_init_slacks": (c_i32, [c_i64, P, P, P, c_dbl, P, P, P, P, P]),
     # batched (K12)
     "gn_ad_eval_batched": (c_i32, [P, c_i32, P, P, P, P, P, P, P, c_i64, P, P, P, P, c_u32, P, P, P]),
     "gn_model_param_count": (c_i32, [P, P]),

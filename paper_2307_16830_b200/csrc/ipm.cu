@@ -264,6 +264,86 @@ __global__ void accept_kernel(int64_t n, int64_t m, gn_ipm_vecs v, gn_vec7 st, d
 
 unsigned ew_blocks(int64_t len) { return static_cast<unsigned>(len > 0 ? (len + 255) / 256 : 1); }
 
+// ---- problem setup: frozen gradient scaling at x0 (ipm.py:179-193),
+// relax_equalities on the scaled ranges (ipm.py:112-123), the start point,
+// the unit bound duals (ipm.py:360-369) and the initial slacks from g(x0)
+// (ipm.py:371-380) -- one elementwise pass each instead of a chain of
+// tensor ops.  The maxima go through atomicMax on the IEEE bits of |v|
+// (non-negative doubles order like their bit patterns, and a NaN bit
+// pattern wins like numpy's max), so they are exact and order-free.
+__device__ __forceinline__ unsigned long long abs_bits(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(fabs(v)));
+}
+__device__ __forceinline__ double nan_max(double a, double b) {   // torch.maximum
+  return (a != a || b != b) ? NAN : (a > b ? a : b);
+}
+__device__ __forceinline__ double nan_min(double a, double b) {   // torch.minimum
+  return (a != a || b != b) ? NAN : (a < b ? a : b);
+}
+__device__ __forceinline__ double unit_scale(double mx) {   // where(mx > 0, min(100 / mx, 1), 1)
+  return mx > 0.0 ? fmin(__ddiv_rn(100.0, mx), 1.0) : 1.0;
+}
+
+__global__ void setup_max_kernel(int64_t n, const double *__restrict__ g0, int64_t nj,
+                                 const double *__restrict__ j0, const int64_t *__restrict__ jrow,
+                                 unsigned long long *bits /* [0] max |g0|, [1 + i] row i max |j0| */) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long gm = 0;
+  for (int64_t i = t0; i < n; i += stride) gm = max(gm, abs_bits(g0[i]));
+  for (int o = 16; o; o >>= 1) gm = max(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+  if ((threadIdx.x & 31) == 0 && gm) atomicMax(bits, gm);
+  for (int64_t t = t0; t < nj; t += stride) {
+    const unsigned long long v = abs_bits(j0[t]);
+    if (v) atomicMax(bits + 1 + jrow[t], v);
+  }
+}
+
+__global__ void setup_vec_kernel(int64_t n, int64_t m, int scaling, double tol,
+                                 const unsigned long long *__restrict__ bits, const double *__restrict__ x0,
+                                 const double *__restrict__ xl, const double *__restrict__ xu,
+                                 const double *__restrict__ rlo, const double *__restrict__ rhi, double *x,
+                                 double *s, double *y, double *zxl, double *zxu, double *zsl, double *zsu,
+                                 double *con_scale, double *sl, double *su, double *obj_scale) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i == 0) *obj_scale = scaling ? unit_scale(__longlong_as_double(static_cast<long long>(bits[0]))) : 1.0;
+  if (i < n) {
+    x[i] = x0[i];
+    zxl[i] = isfinite(xl[i]) ? 1.0 : 0.0;
+    zxu[i] = isfinite(xu[i]) ? 1.0 : 0.0;
+  }
+  if (i < m) {
+    const double cs = scaling ? unit_scale(__longlong_as_double(static_cast<long long>(bits[1 + i]))) : 1.0;
+    con_scale[i] = cs;
+    const double lo = __dmul_rn(rlo[i], cs), hi = __dmul_rn(rhi[i], cs);
+    const double l = isfinite(lo) ? __dsub_rn(lo, __dmul_rn(tol, nan_max(1.0, fabs(lo)))) : -INFINITY;
+    const double u = isfinite(hi) ? __dadd_rn(hi, __dmul_rn(tol, nan_max(1.0, fabs(hi)))) : INFINITY;
+    sl[i] = l;
+    su[i] = u;
+    zsl[i] = isfinite(l) ? 1.0 : 0.0;
+    zsu[i] = isfinite(u) ? 1.0 : 0.0;
+    s[i] = 0.0;
+    y[i] = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+init_slacks_kernel(int64_t m, const double *__restrict__ g, const double *__restrict__ sl,
+                   const double *__restrict__ su, double push_tol, double *s, RedSpec rs) {
+  double acc[1] = {0.0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kRedThreads + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * kRedThreads) {
+    const double l = sl[i], u = su[i];
+    const double lo = isfinite(l) ? __dadd_rn(l, push_tol) : -INFINITY;
+    const double hi = isfinite(u) ? __dsub_rn(u, push_tol) : INFINITY;
+    double s0 = nan_min(nan_max(g[i], lo), hi);
+    if (lo > hi) s0 = __dmul_rn(0.5, __dadd_rn(l, u));
+    s[i] = s0;
+    acc[0] += fabs(__dsub_rn(g[i], s0));
+  }
+  grid_reduce(rs, acc);
+}
+
 }  // namespace
 }  // namespace gn
 
@@ -415,5 +495,38 @@ extern "C" int gn_ipm_accept_batched(gn_kkt *K, int32_t B, const gn_ipm_vecs *v,
   return guarded([&] {
     GN_LAUNCH(accept_kernel, bgrid(ew_blocks(std::max(K->n, K->m)), B), 256, 0, ST(stream), K->n, K->m, *v,
               *steps, 0.0, 0.0, 0.0, kappa_sigma, flags, bx_of(*K, bp));
+  });
+}
+
+extern "C" int gn_ipm_setup(int64_t n, int64_t m, int64_t nj, const double *g0, const double *j0,
+                            const int64_t *jac_rows, const double *x0, const double *xl, const double *xu,
+                            const double *rlo, const double *rhi, int32_t scaling, double tol_r,
+                            uint64_t *scratch, double *x, double *s, double *y, double *zxl, double *zxu,
+                            double *zsl, double *zsu, double *con_scale, double *sl, double *su,
+                            double *obj_scale, void *stream) {
+  return guarded([&] {
+    GN_REQUIRE(n >= 0 && m >= 0 && nj >= 0, "negative size");
+    auto *bits = reinterpret_cast<unsigned long long *>(scratch);
+    GN_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long) * (m + 1), ST(stream)));
+    if (scaling && (n || nj))
+      GN_LAUNCH(setup_max_kernel, ew_blocks(std::max(n, nj)), 256, 0, ST(stream), n, g0, nj, j0, jac_rows, bits);
+    GN_LAUNCH(setup_vec_kernel, ew_blocks(std::max<int64_t>(1, std::max(n, m))), 256, 0, ST(stream), n, m,
+              static_cast<int>(scaling), tol_r, bits, x0, xl, xu, rlo, rhi, x, s, y, zxl, zxu, zsl, zsu,
+              con_scale, sl, su, obj_scale);
+  });
+}
+
+extern "C" int gn_ipm_init_slacks(int64_t m, const double *g, const double *sl, const double *su,
+                                  double push_tol, double *s, double *theta, double *red_partials,
+                                  uint32_t *red_counter, void *stream) {
+  return guarded([&] {
+    if (m <= 0) return;
+    RedSpec r{};
+    r.k = 1;
+    r.op[0] = RED_SUM;
+    r.out = theta;
+    r.partials = red_partials;
+    r.counter = red_counter;
+    GN_LAUNCH(init_slacks_kernel, red_grid(m), kRedThreads, 0, ST(stream), m, g, sl, su, push_tol, s, r);
   });
 }

@@ -232,52 +232,6 @@ class _DeviceSolve:
         dev = D.require_cuda()
         self.dev = dev
         self.obj_scale = 1.0
-        # frozen gradient scaling at x0 (ipm.py:179-193), on the device: the
-        # scale factors, the relaxed slack bounds and the initial slacks are
-        # torch ops; one scalar read later brings obj_scale and theta0 back
-        x0d = pin["x0_d"]
-        g0 = D.empty(n)
-        j0 = D.empty(max(1, model.nnz_jac))
-        self.ev.flags.zero_()
-        self.ev.launch(x0d, GRAD | JAC, grad=g0, jac=j0)
-        self.flags0 = self.ev.flags.clone()
-        self.rlo, self.rhi = pin["rlo"], pin["rhi"]
-        self.rlo_d, self.rhi_d = pin["rlo_d"], pin["rhi_d"]
-        if opts.scaling:
-            gm = g0.abs().max() if n else torch.zeros((), dtype=torch.float64, device=dev)
-            self.obj_scale_d = torch.where(gm > 0, torch.clamp(100.0 / gm, max=1.0), torch.ones_like(gm))
-            if m:
-                rmax = torch.zeros(m, dtype=torch.float64, device=dev)
-                if model.nnz_jac:
-                    rmax.scatter_reduce_(0, model.jac_rows_device(), j0[:model.nnz_jac].abs(), "amax")
-                self.con_scale = torch.where(rmax > 0, torch.clamp(100.0 / rmax, max=1.0),
-                                             torch.ones_like(rmax))
-            else:
-                self.con_scale = D.zeros(1)
-        else:
-            self.obj_scale_d = torch.ones((), dtype=torch.float64, device=dev)
-            self.con_scale = torch.ones(max(1, m), dtype=torch.float64, device=dev)
-        # relax_equalities (ipm.py:112-123) on the scaled ranges
-        if m:
-            tol = self.tol_r
-            rlo_d, rhi_d = pin["rlo_d"], pin["rhi_d"]
-            lo, hi = rlo_d * self.con_scale, rhi_d * self.con_scale
-            one = torch.ones_like(lo)
-            inf = torch.full_like(lo, np.inf)
-            self.sl = torch.where(torch.isfinite(lo), lo - tol * torch.maximum(one, lo.abs()), -inf)
-            self.su = torch.where(torch.isfinite(hi), hi + tol * torch.maximum(one, hi.abs()), inf)
-        else:
-            self.sl, self.su = D.zeros(1), D.zeros(1)
-        self.n_bounds = pin["n_bounds"]
-        self.xl, self.xu = pin["xl_d"], pin["xu_d"]
-        self.x = x0d.clone()
-        self.s, self.y = D.zeros(m), D.zeros(m)
-        fin = lambda t: torch.isfinite(t).to(torch.float64)
-        self.zxl, self.zxu = fin(self.xl), fin(self.xu)
-        self.zsl, self.zsu = (fin(self.sl), fin(self.su)) if m else (D.zeros(0), D.zeros(0))
-        self.grad, self.c = D.empty(n), D.empty(max(1, m))
-        self.dual_x, self.dual_s, self.primal = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
-        self.xt, self.st, self.ct = D.empty(n), D.empty(max(1, m)), D.empty(max(1, m))
         # scalar mailbox: [0:48) prep | 48 f | 49 f_trial | 50.. misc, then the
         # two int32 flag words [AD flags, IPM flags] in the last double, so one
         # copy brings scalars and flags back; the AD kernels write their flags
@@ -290,6 +244,48 @@ class _DeviceSolve:
         self.host = self.host_mail[:96]
         self.host_flags = self.host_mail[96:].view(torch.int32)
         self.stream = torch.cuda.current_stream()
+        # frozen gradient scaling at x0 (ipm.py:179-193), relax_equalities on
+        # the scaled ranges (ipm.py:112-123), the start point and the unit
+        # bound duals, all on the device (gn_ipm_setup); the flags of the
+        # scaling evaluation land in the mailbox's second word and obj_scale
+        # in scal[61], so one read later brings obj_scale, theta0 and both
+        # evaluations' flags back
+        x0d = pin["x0_d"]
+        g0 = D.empty(n)
+        j0 = D.empty(max(1, model.nnz_jac))
+        self.ev.launch(x0d, GRAD | JAC, grad=g0, jac=j0, flags=self.flags[1:2])
+        self.rlo, self.rhi = pin["rlo"], pin["rhi"]
+        self.rlo_d, self.rhi_d = pin["rlo_d"], pin["rhi_d"]
+        self.n_bounds = pin["n_bounds"]
+        self.xl, self.xu = pin["xl_d"], pin["xu_d"]
+        mm = max(1, m)
+        self.x = D.empty(n)
+        self.s, self.y = D.empty(m), D.empty(m)
+        self.zxl, self.zxu = D.empty(n), D.empty(n)
+        self.zsl, self.zsu = D.empty(m), D.empty(m)
+        self.con_scale, self.sl, self.su = D.empty(mm), D.empty(mm), D.empty(mm)
+        if not m:   # placeholders the kernels never read
+            self.con_scale.fill_(0.0 if opts.scaling else 1.0)
+            self.sl.zero_()
+            self.su.zero_()
+        bits = torch.empty(m + 1, dtype=torch.int64, device=dev)
+        L.check(L.lib().gn_ipm_setup(
+            n, m, model.nnz_jac, L.ptr(g0), L.ptr(j0),
+            L.ptr(model.jac_rows_device()) if model.nnz_jac else None, L.ptr(x0d), L.ptr(self.xl),
+            L.ptr(self.xu), L.ptr(self.rlo_d), L.ptr(self.rhi_d), 1 if opts.scaling else 0,
+            float(self.tol_r), L.ptr(bits), L.ptr(self.x), L.ptr(self.s), L.ptr(self.y), L.ptr(self.zxl),
+            L.ptr(self.zxu), L.ptr(self.zsl), L.ptr(self.zsu), L.ptr(self.con_scale), L.ptr(self.sl),
+            L.ptr(self.su), L.ptr(self.scal[61:62]), D.stream_ptr()))
+        self.grad, self.c = D.empty(n), D.empty(mm)
+        self.dual_x, self.dual_s, self.primal = D.empty(n), D.empty(mm), D.empty(mm)
+        self.xt, self.st, self.ct = D.empty(n), D.empty(mm), D.empty(mm)
+        # reduction scratch of the initial-slack sum (counter left zeroed)
+        red = model.__dict__.get("_setup_red")
+        if red is None or red[0].device != dev:
+            red = (torch.empty(L.GN_RED_PARTIALS, dtype=torch.float64, device=dev),
+                   torch.zeros(1, dtype=torch.int32, device=dev))
+            model.__dict__["_setup_red"] = red
+        self.red = red
 
     def vecs(self, ws) -> L.IpmVecs:
         return L.IpmVecs(*(t.data_ptr() for t in (
@@ -453,23 +449,15 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             raise DegenerateInterior("s slack lost strict interiority")
 
     # initial slacks from g(x0) (ipm.py:371-380), on the device; one read
-    # returns obj_scale, theta0 and the flags of both evaluations at x0
-    P.flags.zero_()
+    # returns obj_scale, theta0 and the flags of both evaluations at x0 (the
+    # mailbox is fresh: both flag words start at zero)
     t0 = timer.start()
     ev.launch(P.x, C, con_scale=P.con_scale, c=P.c, flags=P.flag_ad)
     timer.stop("ad", t0)
     if m:
-        tol_r, push = P.tol_r, opts.bound_push
-        g0 = P.c[:m]
-        inf = torch.full_like(g0, np.inf)
-        lo = torch.where(torch.isfinite(P.sl), P.sl + push * tol_r, -inf)
-        hi = torch.where(torch.isfinite(P.su), P.su - push * tol_r, inf)
-        s0 = torch.minimum(torch.maximum(g0, lo), hi)
-        s0 = torch.where(lo > hi, 0.5 * (P.sl + P.su), s0)
-        P.s.copy_(s0)
-        P.scal[60] = (g0 - s0).abs().sum()
-    P.scal[61] = P.obj_scale_d
-    P.flags[1:2].copy_(P.flags0)
+        L.check(lib.gn_ipm_init_slacks(m, L.ptr(P.c), L.ptr(P.sl), L.ptr(P.su),
+                                       opts.bound_push * P.tol_r, L.ptr(P.s), L.ptr(P.scal[60:61]),
+                                       L.ptr(P.red[0]), L.ptr(P.red[1]), stream))
     sc0, adf0, adf_x0 = P.read(60, 62)
     if adf_x0:
         # the scaling evaluations at x0 failed: _Problem's constructor raised
