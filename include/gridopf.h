@@ -34,6 +34,8 @@ const char *gn_last_error(void);
 int gn_version(void);
 /* kernel launches and plan-upload bytes since the last reset */
 void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset);
+/* plan-upload host time, recorded only with GN_HOST_TIMING=1 (diagnostics) */
+void gn_upload_stats(int64_t *n_alloc, double *malloc_ms, double *copy_ms, int reset);
 /* Host threads the calling thread's structure analysis (condense, ordering
  * support, symbolic factor, front plan) may use; <= 0 restores the default.
  * Thread-local (an analysis worker leaves a core to the launching thread). */

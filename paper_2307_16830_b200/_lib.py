@@ -92,6 +92,7 @@ _SIGS = {
     "gn_chol_set_trace": (c_i32, [P, P]),
     "gn_set_concurrency": (c_i32, [c_i32]),
     "gn_alloc_trim": (c_i32, [P]),
+    "gn_upload_stats": (None, [P, P, P, c_i32]),
     "gn_symbolic_fronts": (c_i32, [P, P, P, P, P, P, P]),
     "gn_kkt_create": (c_i32, [c_i64, c_i64, c_i64, P, P, c_i64, P, P, P, P]),
     "gn_kkt_destroy": (None, [P]),

@@ -69,6 +69,19 @@ extern "C" int gn_set_host_threads(int k) {
   return 0;
 }
 
+// plan-upload host time (GN_HOST_TIMING=1 only): device allocations and
+// their time, H2D copy time; diagnostics
+extern "C" void gn_upload_stats(int64_t *n_alloc, double *malloc_ms, double *copy_ms, int reset) {
+  if (n_alloc) *n_alloc = gn::g_nalloc.load();
+  if (malloc_ms) *malloc_ms = 1e-6 * static_cast<double>(gn::g_malloc_ns.load());
+  if (copy_ms) *copy_ms = 1e-6 * static_cast<double>(gn::g_copy_ns.load());
+  if (reset) {
+    gn::g_nalloc.store(0);
+    gn::g_malloc_ns.store(0);
+    gn::g_copy_ns.store(0);
+  }
+}
+
 extern "C" void gn_stats(int64_t *launches, int64_t *h2d_bytes, int reset) {
   if (launches) *launches = gn::g_launches.load();
   if (h2d_bytes) *h2d_bytes = gn::g_h2d.load();

@@ -20,13 +20,19 @@ for nt in [int(a) for a in sys.argv[1:]] or [16]:
     _lib.lib().gn_set_host_threads(nt)
     opts = SolverOptions(tol=1e-6, ordering=perm)
     walls = []
+    import ctypes
     for r in range(6):
         model.release_device()
         torch.cuda.synchronize()
+        _lib.lib().gn_upload_stats(None, None, None, 1)
         t = time.perf_counter()
         rep = solve(model, opts, constraint_ranges=am.ranges)
         torch.cuda.synchronize()
         walls.append(time.perf_counter() - t)
+        na, mm, cm = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        _lib.lib().gn_upload_stats(ctypes.byref(na), ctypes.byref(mm), ctypes.byref(cm), 0)
+        print(f"  solve {r}: {walls[-1]*1e3:.1f} ms, allocs {na.value} malloc {mm.value:.2f} ms copies {cm.value:.2f} ms",
+              flush=True)
     s = rep.debug["setup_seconds"]
     print(f"threads {nt}: wall {min(walls)*1e3:.1f} ms  ipm_total {rep.seconds['total']*1e3:.1f}  setup",
           {k: round(v * 1e3, 2) for k, v in s.items()}, flush=True)
