@@ -561,7 +561,7 @@ void Symbolic::ensure_l_export() {
     std::vector<int32_t> pos(n, -1);
 #pragma omp for schedule(dynamic, 64)
     for (int64_t J = 0; J < nf; ++J) {
-      const int64_t r0 = f_rows_off[J], r1 = f_rows_off[J + 1], sJ = f_nrows[J];
+      const int64_t r0 = f_rows_off[J], r1 = f_rows_off[J + 1], sJ = front_ld(f_nrows[J]);
       for (int64_t q = r0; q < r1; ++q) pos[f_rows[q]] = static_cast<int32_t>(q - r0);
       for (int64_t j = f_first[J]; j < f_first[J] + f_ncols[J]; ++j) {
         const int64_t base = f_off[J] + (j - f_first[J]) * sJ;
@@ -638,7 +638,7 @@ static void front_plan(Symbolic &S) {
     int64_t s = w + cc[l] - 1;
     S.f_nrows[J] = static_cast<int32_t>(s);
     S.f_rows_off[J + 1] = S.f_rows_off[J] + s;
-    S.f_off[J + 1] = S.f_off[J] + s * s;
+    S.f_off[J + 1] = S.f_off[J] + s * front_ld(s);   // even ld: 16-byte aligned columns
     S.f_voff[J + 1] = S.f_voff[J] + s;
     S.max_front = std::max(S.max_front, s);
     S.max_cols = std::max(S.max_cols, w);
@@ -716,7 +716,7 @@ static void front_plan(Symbolic &S) {
     for (int64_t J = 0; J < nf; ++J) {
       const int64_t r0 = S.f_rows_off[J], r1 = S.f_rows_off[J + 1];
       for (int64_t q = r0; q < r1; ++q) pos[S.f_rows[q]] = static_cast<int32_t>(q - r0);
-      const int64_t sJ = S.f_nrows[J];
+      const int64_t sJ = front_ld(S.f_nrows[J]);
       auto local = [&](int64_t row) -> int64_t {
         const int32_t v = pos[row];
         missing |= v < 0;

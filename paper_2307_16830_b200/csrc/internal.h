@@ -197,6 +197,10 @@ struct Condense {
 };
 
 // ------------------------------------------------------- symbolic factor
+// leading dimension of a front's column-major storage: even, so that with
+// even front offsets every column starts 16-byte aligned (bulk copies)
+inline int64_t front_ld(int64_t s) { return s + (s & 1); }
+
 constexpr int kWarpFrontRows = 32;   // fronts this small are factored by one warp
 constexpr int kTopFronts = 24;       // at most this many top fronts go to the cluster kernel
 constexpr int kTopMinRows = 96;      // ... and only fronts at least this tall
