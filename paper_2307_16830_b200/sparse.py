@@ -288,7 +288,7 @@ def trace_factor_solve(symbolic: SymbolicFactorization, kvals: torch.Tensor, b: 
     [64][5] panel stamps of the last front (start, loaded, diagonal block,
     TRSM, trailing update)."""
     nf = symbolic.info["n_fronts"]
-    tr = torch.zeros(3 * nf * 4 + 64 * 5, dtype=torch.int64, device=kvals.device)
+    tr = torch.zeros(3 * nf * 4 + 64 * 5 + 256, dtype=torch.int64, device=kvals.device)
     h = symbolic.handle()
     L.check(L.lib().gn_chol_set_trace(h, L.ptr(tr)))
     try:
@@ -298,4 +298,5 @@ def trace_factor_solve(symbolic: SymbolicFactorization, kvals: torch.Tensor, b: 
     finally:
         L.check(L.lib().gn_chol_set_trace(h, None))
     t = tr.cpu().numpy()
-    return t[:12 * nf].reshape(3, nf, 4), t[12 * nf:].reshape(64, 5)
+    trace_factor_solve.last_probes = t[12 * nf + 320:]   # kernel-specific probe stamps (diagnostics)
+    return t[:12 * nf].reshape(3, nf, 4), t[12 * nf:12 * nf + 320].reshape(64, 5)
