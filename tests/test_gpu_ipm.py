@@ -117,3 +117,57 @@ def test_regularization_inside_solve_matches_oracle(tol):
     assert dws == [row[6] for row in orep.trace]
     assert rep.objective == pytest.approx(orep.objective, rel=1e-9, abs=1e-12)
     np.testing.assert_allclose(rep.x, orep.x, atol=1e-7)
+
+
+@pytest.mark.parametrize("scaling", (True, False))
+def test_native_setup_matches_oracle(networks_json, scaling):
+    """gn_ipm_setup / gn_ipm_init_slacks vs the oracle's restatement of the
+    _Problem scaling, relax_equalities and the initial slacks
+    (ipm.py:112-123, 179-193, 371-380): bitwise for the scales, bounds,
+    duals and slacks; theta0 (a sum) within 1e-14."""
+    import torch
+
+    from oracle import ipm as OI
+    from oracle import model as OM
+    from paper_2307_16830_b200.acopf import build_acopf
+    from paper_2307_16830_b200.matpower import network_from_tables
+
+    am = build_acopf(network_from_tables(networks_json["case118"]))
+    m_ = am.model
+    opts = SolverOptions(tol=1e-6, max_iter=0, scaling=scaling, keep_workspace=True)
+    rep = solve(m_, opts, constraint_ranges=am.ranges)
+    P = rep.debug["problem"]
+    om = OM.expand(m_.n_var, m_.n_con, OM.from_model(m_))
+    xl, xu, x0 = P.xl_h, P.xu_h, P.x0
+    n, m = m_.n_var, m_.n_con
+    if scaling:
+        g0 = OM.gradient(om, x0)
+        j0 = OM.jacobian(om, x0)
+        gm = np.abs(g0).max()
+        osc = min(1.0, 100.0 / gm) if gm > 0 else 1.0
+        rmax = np.zeros(m)
+        np.maximum.at(rmax, om.jac_rows, np.abs(j0))
+        csc = np.ones(m)
+        pos = rmax > 0
+        csc[pos] = np.minimum(1.0, 100.0 / rmax[pos])
+    else:
+        osc, csc = 1.0, np.ones(m)
+    host = lambda t: t.detach().cpu().numpy()[:m]
+    # the scales from device AD values (AD parity is 1e-12, not bitwise)
+    assert P.obj_scale == pytest.approx(osc, rel=1e-12)
+    np.testing.assert_allclose(host(P.con_scale), csc, rtol=1e-12)
+    # the rest bitwise from the device's own scales and g(x0)
+    csc_d = host(P.con_scale)
+    ranges = np.asarray(am.ranges, float)
+    sl, su = OI.relax_equalities(m, np.column_stack([ranges[:, 0] * csc_d, ranges[:, 1] * csc_d]), P.tol_r)
+    np.testing.assert_array_equal(host(P.sl), sl)
+    np.testing.assert_array_equal(host(P.su), su)
+    np.testing.assert_array_equal(P.x.cpu().numpy(), x0)
+    np.testing.assert_array_equal(host(P.zsl), np.isfinite(sl).astype(float))
+    np.testing.assert_array_equal(P.zxu.cpu().numpy(), np.isfinite(xu).astype(float))
+    g = host(P.c)
+    s0 = OI.initial_slacks(g, sl, su, P.tol_r, opts.bound_push)
+    np.testing.assert_array_equal(host(P.s), s0)
+    theta0 = float(P.scal[60].item())
+    assert theta0 == pytest.approx(float(np.abs(g - s0).sum()), rel=1e-14)
+    torch.cuda.synchronize()
