@@ -53,9 +53,9 @@ T *dev_alloc(size_t count) {
   return static_cast<T *>(dev_malloc(sizeof(T) * (count ? count : 1)));
 }
 
-template <class D, class S>
-std::vector<D> narrow(const std::vector<S> &v) {
-  std::vector<D> out(v.size());
+template <class D, class S, class A>
+uvec<D> narrow(const std::vector<S, A> &v) {
+  uvec<D> out(v.size());
   for (size_t i = 0; i < v.size(); ++i) out[i] = static_cast<D>(v[i]);
   return out;
 }

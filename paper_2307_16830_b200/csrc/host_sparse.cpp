@@ -426,7 +426,7 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
     pinv[perm[k]] = k;
   }
   PhaseTimer tm_perm("symbolic.permute+sort");
-  std::vector<int64_t> prow(nnz), pcol(nnz);
+  uvec<int64_t> prow(nnz), pcol(nnz);
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t j = 0; j < n; ++j)
     for (int64_t p = indptr[j]; p < indptr[j + 1]; ++p) {
@@ -436,7 +436,7 @@ static void symbolic(Symbolic &S, int64_t n, const int64_t *indptr, const int64_
     }
   // order by (prow, pcol): bucket by prow, then sort each row by pcol (the
   // pairs are unique, so this is the reference's stable lexicographic order)
-  std::vector<int64_t> o2(nnz);
+  uvec<int64_t> o2(nnz);
   par_bucket(n, nnz, [&](int64_t p) { return prow[p]; }, [&](int64_t p, int64_t d) { o2[d] = p; },
              S.a_rowptr);
   S.a_rowcol.resize(nnz);
@@ -648,13 +648,13 @@ static void front_plan(Symbolic &S) {
   {
     PhaseTimer tm_rows("front_plan.rows");
     const int64_t nrc = S.row_ptr[n];
-    std::vector<int32_t> rowof(nrc);
+    uvec<int32_t> rowof(nrc);
 #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t k = 0; k < n; ++k)
       for (int64_t t = S.row_ptr[k]; t < S.row_ptr[k + 1]; ++t) rowof[t] = static_cast<int32_t>(k);
     std::vector<int64_t> sptr;
-    S.f_rows.assign(S.f_rows_off[nf], 0);
-    std::vector<int32_t> srow(S.f_rows_off[nf]);   // >= the struct entries
+    S.f_rows.resize(S.f_rows_off[nf]);             // every entry written below
+    uvec<int32_t> srow(S.f_rows_off[nf]);          // >= the struct entries
     par_bucket(nf + 1, nrc,
                [&](int64_t t) { const int32_t J = last_of[S.row_cols[t]]; return J >= 0 ? J : nf; },
                [&](int64_t t, int64_t d) {
@@ -687,11 +687,11 @@ static void front_plan(Symbolic &S) {
   PhaseTimer tm_maps("front_plan.maps");
   // A entries grouped by front (ascending row inside a front)
   const int64_t na = S.a_rowptr[n];
-  std::vector<int32_t> arow(na);
+  uvec<int32_t> arow(na);
 #pragma omp parallel for schedule(dynamic, 1024)
   for (int64_t k = 0; k < n; ++k)
     for (int64_t t = S.a_rowptr[k]; t < S.a_rowptr[k + 1]; ++t) arow[t] = static_cast<int32_t>(k);
-  std::vector<int64_t> a_t(na);
+  uvec<int64_t> a_t(na);
   par_bucket(nf, na, [&](int64_t t) { return snode_of[S.a_rowcol[t]]; },
              [&](int64_t t, int64_t d) { a_t[d] = t; }, S.f_a_ptr);
   const std::vector<int64_t> &per = S.f_a_ptr;
@@ -702,9 +702,9 @@ static void front_plan(Symbolic &S) {
     if (S.f_parent[C] < 0) GN_REQUIRE(sC == w, "root front with an update block");
     S.f_relmap_off[C + 1] = S.f_relmap_off[C] + (S.f_parent[C] >= 0 ? sC - w : 0);
   }
-  S.relmap.assign(S.f_relmap_off[nf], 0);
-  S.a_kslot.assign(na, 0);
-  S.a_fpos.assign(na, 0);
+  S.relmap.resize(S.f_relmap_off[nf]);   // every entry written below
+  S.a_kslot.resize(na);
+  S.a_fpos.resize(na);
   // local row positions through a dense per-thread position map filled per
   // front (O(1) lookups); every front writes disjoint ranges (its own A
   // entries, its columns of L, its children's relmaps)

@@ -217,7 +217,8 @@ struct alignas(16) FrontMeta {
 
 struct Symbolic {
   int64_t n = 0, nnz_a = 0, nnz_l = 0;
-  std::vector<int64_t> perm, parent, a_rowptr, a_rowcol, a_srcslot, row_ptr, l_colptr;
+  std::vector<int64_t> perm, parent, a_rowptr, row_ptr, l_colptr;
+  uvec<int64_t> a_rowcol, a_srcslot;
   uvec<int64_t> row_cols;   // row patterns of L, each row in etree-reach order
   // the reference L row indices (CSC) and the L -> front map are only needed
   // for exports: built on first use (ensure_l_csc / ensure_l_export)
@@ -229,14 +230,14 @@ struct Symbolic {
   int64_t nf = 0;                              // number of fronts
   std::vector<int32_t> f_first, f_ncols, f_nrows, f_parent;
   std::vector<int64_t> f_rows_off;             // into f_rows
-  std::vector<int32_t> f_rows;                 // sorted internal row indices per front
+  uvec<int32_t> f_rows;                        // sorted internal row indices per front
   std::vector<int64_t> f_off;                  // F storage offset (doubles)
   std::vector<int64_t> f_voff;                 // solve scratch offset (doubles)
   std::vector<int32_t> f_child_ptr, f_child;   // CSR children
   std::vector<int64_t> f_relmap_off;           // per front: r entries into relmap
-  std::vector<int32_t> relmap;                 // child update rows -> parent local rows
+  uvec<int32_t> relmap;                        // child update rows -> parent local rows
   std::vector<int64_t> f_a_ptr;                // CSR A scatter per front
-  std::vector<int64_t> a_kslot, a_fpos;        // (kvals slot, F offset)
+  uvec<int64_t> a_kslot, a_fpos;               // (kvals slot, F offset)
   std::vector<int32_t> order;                  // task order: [small by level | large by level]
   int64_t nf_small = 0;                        // warp-task fronts (prefix of order)
   int64_t nf_top = 0;                          // cluster-task fronts (suffix of order)
