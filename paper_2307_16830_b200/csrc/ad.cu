@@ -409,11 +409,22 @@ Model::~Model() { release_model(*this); }
 
 static void upload_model(Model &M) {
   PhaseTimer tm("upload_model");
+  PhaseTimer tm_b("upload_model.blocks");
   std::vector<DevBlock> db;
   std::vector<int4> tape;
   std::vector<double> consts;
-  std::vector<int32_t> slots, vidx, tg;
-  std::vector<double> par;
+  std::vector<int32_t> slots;
+  // the record arrays (SoA, slot-major) are sized first and filled in
+  // parallel: they are the bulk of the plan
+  int64_t nvid = 0, npar = 0, ntg = 0;
+  for (auto &b : M.blocks) {
+    nvid += b.R * b.nv;
+    npar += b.R * b.np;
+    ntg += static_cast<int64_t>(b.targets.size());
+  }
+  uvec<int32_t> vidx(nvid), tg(ntg);
+  uvec<double> par(npar);
+  int64_t ovid = 0, opar = 0, otg = 0;
   int64_t cta = 0, coff = 0;
   for (auto &b : M.blocks) {
     DevBlock d{};
@@ -425,9 +436,9 @@ static void upload_model(Model &M) {
     d.nfirst = static_cast<int32_t>(b.first.size());
     d.npairs = static_cast<int32_t>(b.pairs.size() / 2);
     d.R = b.R;
-    d.var_off = static_cast<int64_t>(vidx.size());
-    d.par_off = static_cast<int64_t>(par.size());
-    d.tgt_off = static_cast<int64_t>(tg.size());
+    d.var_off = ovid;
+    d.par_off = opar;
+    d.tgt_off = otg;
     d.contrib_off = coff;
     coff += b.R * (1 + d.nfirst + d.npairs);
     d.tape_off = static_cast<int32_t>(tape.size());
@@ -449,15 +460,27 @@ static void upload_model(Model &M) {
     std::sort(sw.begin(), sw.end());
     d.nsweep = static_cast<int32_t>(sw.size());
     for (int s : sw) slots.push_back(s);
-    for (int s = 0; s < b.nv; ++s)
-      for (int64_t r = 0; r < b.R; ++r) vidx.push_back(static_cast<int32_t>(b.var_idx[r * b.nv + s]));
-    for (int s = 0; s < b.np; ++s)
-      for (int64_t r = 0; r < b.R; ++r) par.push_back(b.params[r * b.np + s]);
-    for (int64_t r = 0; r < static_cast<int64_t>(b.targets.size()); ++r) tg.push_back(static_cast<int32_t>(b.targets[r]));
+    const int64_t R = b.R, nv = b.nv, npb = b.np, nt = static_cast<int64_t>(b.targets.size());
+    int32_t *vo = vidx.data() + ovid;
+    double *po = par.data() + opar;
+    int32_t *to = tg.data() + otg;
+#pragma omp parallel for schedule(static) if (R > 16384)
+    for (int64_t r = 0; r < R; ++r) {
+      for (int64_t q = 0; q < nv; ++q) vo[q * R + r] = static_cast<int32_t>(b.var_idx[r * nv + q]);
+      for (int64_t q = 0; q < npb; ++q) po[q * R + r] = b.params[r * npb + q];
+      if (r < nt) to[r] = static_cast<int32_t>(b.targets[r]);
+    }
+    for (int64_t r = R; r < nt; ++r) to[r] = static_cast<int32_t>(b.targets[r]);
+    ovid += R * nv;
+    opar += R * npb;
+    otg += nt;
     db.push_back(d);
   }
+  tm_b.~PhaseTimer();
+  new (&tm_b) PhaseTimer("upload_model.blocks_done");
   GN_REQUIRE(coff == M.n_contrib, "contribution layout mismatch");
   GN_REQUIRE(coff < (int64_t(1) << 31), "contribution array too large for int32 gather lists");
+  PhaseTimer tm_up("upload_model.copies");
   M.dblocks = db;
   M.n_ctas_rec = cta;
   M.d.blocks = dev_upload(db);
@@ -480,9 +503,11 @@ static void upload_model(Model &M) {
   M.d.obj_partials = dev_alloc<double>(kObjMaxCtas);
   M.d.obj_counter = dev_upload(std::vector<unsigned>{0u});
   M.batch_cap = 1;
-  M.n_params = static_cast<int64_t>(par.size());
+  M.n_params = npar;
   M.d.n_obj_blocks = static_cast<int32_t>(M.obj_block_ptr.size()) - 1;
   M.d.jac_rows = dev_upload(narrow<int32_t>(M.jac_rows));
+  tm_up.~PhaseTimer();
+  new (&tm_up) PhaseTimer("upload_model.rest");
   // pattern kernels generated from the tapes (NVRTC, cached per source)
   M.pattern_fn = nullptr;
   const char *env = std::getenv("GN_AD_INTERPRETER");

@@ -401,7 +401,7 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
     rowptr[jr[p] + 1]++;
   }
   for (int64_t i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
-  std::vector<int32_t> col(nj), at_p(nj), at_row(nj);
+  uvec<int32_t> col(nj), at_p(nj), at_row(nj);
   for (int64_t p = 0; p < nj; ++p) col[p] = static_cast<int32_t>(jc[p]);
   std::vector<int64_t> atptr(n + 1, 0);
   for (int64_t p = 0; p < nj; ++p) atptr[jc[p] + 1]++;
@@ -422,7 +422,7 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
     if (hr[p] != hc[p]) wptr[hc[p] + 1]++;
   }
   for (int64_t i = 0; i < n; ++i) wptr[i + 1] += wptr[i];
-  std::vector<int32_t> wp(wptr[n]), wj(wptr[n]);
+  uvec<int32_t> wp(wptr[n]), wj(wptr[n]);
   {
     std::vector<int64_t> fl(wptr.begin(), wptr.end() - 1);
     for (int64_t p = 0; p < nh; ++p) {
@@ -437,6 +437,7 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
         wj[q] = static_cast<int32_t>(hr[p]);
       }
   }
+  PhaseTimer tm_up("kkt_create.copies");
   K.d.a_rowptr = dev_upload(rowptr);
   K.d.a_col = dev_upload(col);
   K.d.at_ptr = dev_upload(atptr);
