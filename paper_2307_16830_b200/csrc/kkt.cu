@@ -85,6 +85,53 @@ __device__ __forceinline__ dd dd_gather_dot(int64_t t0, int64_t t1, const double
   return acc;
 }
 
+// Two gathered double-double dot products with their first four terms each
+// in flight together (indices of both, then values of both), then the rest
+// in chunks of four; each sum accumulates in ascending t as dd_gather_dot.
+template <class IA1, class IB1, class IA2, class IB2>
+__device__ __forceinline__ void dd_gather_dot2(int64_t s0, int64_t s1, const double *__restrict__ a1, IA1 ia1,
+                                               const double *__restrict__ b1, IB1 ib1, int64_t u0, int64_t u1,
+                                               const double *__restrict__ a2, IA2 ia2,
+                                               const double *__restrict__ b2, IB2 ib2, dd &r1, dd &r2) {
+  int64_t p1[4], q1[4], p2[4], q2[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    p1[u] = s0 + u < s1 ? ia1(s0 + u) : 0;
+    q1[u] = s0 + u < s1 ? ib1(s0 + u) : 0;
+    p2[u] = u0 + u < u1 ? ia2(u0 + u) : 0;
+    q2[u] = u0 + u < u1 ? ib2(u0 + u) : 0;
+  }
+  double x1[4], y1[4], x2[4], y2[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    x1[u] = s0 + u < s1 ? a1[p1[u]] : 0.0;
+    y1[u] = s0 + u < s1 ? b1[q1[u]] : 0.0;
+    x2[u] = u0 + u < u1 ? a2[p2[u]] : 0.0;
+    y2[u] = u0 + u < u1 ? b2[q2[u]] : 0.0;
+  }
+  r1 = {0.0, 0.0};
+  r2 = {0.0, 0.0};
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (s0 + u < s1) r1 = dd_add(r1, dd_prod(x1[u], y1[u]));
+    if (u0 + u < u1) r2 = dd_add(r2, dd_prod(x2[u], y2[u]));
+  }
+  for (int64_t t = s0 + 4; t < s1; t += 4) {
+    double va[4], vb[4];
+    gather4(t, s1, a1, ia1, b1, ib1, va, vb);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t + u < s1) r1 = dd_add(r1, dd_prod(va[u], vb[u]));
+  }
+  for (int64_t t = u0 + 4; t < u1; t += 4) {
+    double va[4], vb[4];
+    gather4(t, u1, a2, ia2, b2, ib2, va, vb);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t + u < u1) r2 = dd_add(r2, dd_prod(va[u], vb[u]));
+  }
+}
+
 // W v from the lower triangle: first every entry's row contribution, then
 // the mirrored off-diagonal contributions (kkt.py:132-138)
 __global__ void w_matvec_kernel(int64_t n, const int64_t *ptr, const int32_t *wp, const int32_t *wj,
@@ -254,10 +301,10 @@ __global__ void residual_x_kernel(int64_t n, const int64_t *wptr, const int32_t 
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; j < n;
        j += static_cast<int64_t>(gridDim.x) * kT) {
     const double dxj = step.x[j];
-    const dd wv = dd_gather_dot(wptr[j], wptr[j + 1], st.w, [&](int64_t t) { return wp[t]; }, step.x,
-                                [&](int64_t t) { return wj[t]; });
-    const dd atv = dd_gather_dot(atptr[j], atptr[j + 1], st.a, [&](int64_t t) { return atp[t]; }, step.y,
-                                 [&](int64_t t) { return atrow[t]; });
+    dd wv, atv;
+    dd_gather_dot2(wptr[j], wptr[j + 1], st.w, [&](int64_t t) { return wp[t]; }, step.x,
+                   [&](int64_t t) { return wj[t]; }, atptr[j], atptr[j + 1], st.a,
+                   [&](int64_t t) { return atp[t]; }, step.y, [&](int64_t t) { return atrow[t]; }, wv, atv);
     dd rx = dd_from(pv.x[j]);
     rx = dd_add(rx, dd_neg(wv));
     rx = dd_add(rx, dd_neg(dd_prod(st.dw, dxj)));

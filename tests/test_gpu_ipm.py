@@ -171,3 +171,42 @@ def test_native_setup_matches_oracle(networks_json, scaling):
     theta0 = float(P.scal[60].item())
     assert theta0 == pytest.approx(float(np.abs(g - s0).sum()), rel=1e-14)
     torch.cuda.synchronize()
+
+
+def test_resolve_after_input_changes_matches_fresh_model(networks_json):
+    """Cached per-model state (prepared inputs, symbolic plans keyed on the
+    ordering's content) is invalidated by changed inputs: re-solving the same
+    model object after changing its start point, its ranges, or mutating the
+    ordering array in place equals a solve of a freshly built model."""
+    from paper_2307_16830_b200 import kkt as K
+    from paper_2307_16830_b200 import sparse as S
+    from paper_2307_16830_b200.acopf import build_acopf
+    from paper_2307_16830_b200.matpower import network_from_tables
+
+    build = lambda: build_acopf(network_from_tables(networks_json["case30"]))
+    am = build()
+    opts = SolverOptions(tol=1e-6)
+    solve(am.model, opts, constraint_ranges=am.ranges)
+    rng = np.random.default_rng(5)
+    am.model.start[:] = am.model.start + 0.01 * rng.random(am.model.n_var)
+    ranges2 = np.array(am.ranges, dtype=float)
+    ineq = ranges2[:, 0] != ranges2[:, 1]
+    ranges2[ineq] *= 0.9
+    r1 = solve(am.model, opts, constraint_ranges=ranges2)
+    fresh = build()
+    fresh.model.start[:] = am.model.start
+    r2 = solve(fresh.model, opts, constraint_ranges=ranges2)
+    assert (r1.status, r1.iterations) == (r2.status, r2.iterations)
+    assert r1.objective == r2.objective
+    np.testing.assert_array_equal(r1.x, r2.x)
+    # ordering: the same array object mutated in place is a new ordering
+    m_ = am.model
+    cs = K.symbolic_condense(m_.hess_rows, m_.hess_cols, m_.jac_rows, m_.jac_cols, m_.n_var)
+    perm = S.amd_order(cs.matrix)
+    solve(m_, SolverOptions(tol=1e-6, ordering=perm), constraint_ranges=ranges2)
+    perm[[0, -1]] = perm[[-1, 0]]
+    r3 = solve(m_, SolverOptions(tol=1e-6, ordering=perm), constraint_ranges=ranges2)
+    r4 = solve(fresh.model, SolverOptions(tol=1e-6, ordering=perm.copy()), constraint_ranges=ranges2)
+    assert (r3.status, r3.iterations) == (r4.status, r4.iterations)
+    assert r3.objective == r4.objective
+    np.testing.assert_array_equal(r3.x, r4.x)
