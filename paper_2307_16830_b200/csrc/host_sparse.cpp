@@ -213,8 +213,10 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
   // Jacobian entries by column (ascending entry, hence ascending row) and
   // W entries by column (input order)
   PhaseTimer tm_b("condense.buckets");
-  std::vector<int64_t> aptr, hptr;
-  std::vector<int32_t> alist(nj), hlist(nh);
+  std::vector<int64_t> &aptr = C.a_colptr, hptr;
+  uvec<int32_t> &alist = C.a_colent;
+  uvec<int32_t> hlist(nh);
+  alist.resize(nj);
   par_bucket(n, nj, [&](int64_t p) { return jc[p]; },
              [&](int64_t p, int64_t d) { alist[d] = static_cast<int32_t>(p); }, aptr);
   par_bucket(n, nh, [&](int64_t t) { return hc[t]; },

@@ -185,6 +185,9 @@ struct Condense {
   // constraint row; one trailing entry
   std::vector<int64_t> seg, seg_poff, seg_row;
   uvec<int32_t> k_ptr, k_row, k_s1, k_s2;   // products grouped by K slot
+  // the Jacobian by column (entries ascending): A^T's CSR, reused by the KKT plan
+  std::vector<int64_t> a_colptr;
+  uvec<int32_t> a_colent;
   bool plan_built = false;
   std::mutex plan_mu;
   void ensure_assembly_plan();

@@ -442,18 +442,38 @@ static void kkt_create(Kkt &K, int64_t n, int64_t m, int64_t nh, const int64_t *
   K.nj = nj;
   // A rows (jac is row-major sorted)
   std::vector<int64_t> rowptr(m + 1, 0);
-  for (int64_t p = 0; p < nj; ++p) {
-    GN_REQUIRE(jr[p] >= 0 && jr[p] < m && jc[p] >= 0 && jc[p] < n, "Jacobian index out of range");
-    GN_REQUIRE(p == 0 || jr[p] >= jr[p - 1], "Jacobian must be sorted by row");
-    rowptr[jr[p] + 1]++;
+  const bool have_segs = cs && cs->nnz_j == nj && cs->n == n && !cs->seg.empty();
+  if (have_segs) {
+    // the condensation checked the order and the columns and split the
+    // Jacobian into row segments: the row pointers from the segments
+    const int64_t nseg = static_cast<int64_t>(cs->seg.size()) - 1;
+    for (int64_t g = 0; g < nseg; ++g) {
+      GN_REQUIRE(cs->seg_row[g] >= 0 && cs->seg_row[g] < m, "Jacobian index out of range");
+      rowptr[cs->seg_row[g] + 1] = cs->seg[g + 1] - cs->seg[g];
+    }
+  } else {
+    for (int64_t p = 0; p < nj; ++p) {
+      GN_REQUIRE(jr[p] >= 0 && jr[p] < m && jc[p] >= 0 && jc[p] < n, "Jacobian index out of range");
+      GN_REQUIRE(p == 0 || jr[p] >= jr[p - 1], "Jacobian must be sorted by row");
+      rowptr[jr[p] + 1]++;
+    }
   }
   for (int64_t i = 0; i < m; ++i) rowptr[i + 1] += rowptr[i];
   uvec<int32_t> col(nj), at_p(nj), at_row(nj);
   for (int64_t p = 0; p < nj; ++p) col[p] = static_cast<int32_t>(jc[p]);
-  std::vector<int64_t> atptr(n + 1, 0);
-  for (int64_t p = 0; p < nj; ++p) atptr[jc[p] + 1]++;
-  for (int64_t j = 0; j < n; ++j) atptr[j + 1] += atptr[j];
-  {
+  std::vector<int64_t> atptr;
+  if (cs && static_cast<int64_t>(cs->a_colptr.size()) == n + 1 &&
+      static_cast<int64_t>(cs->a_colent.size()) == nj) {
+    // the condensation already bucketed the Jacobian by column (same order)
+    atptr = cs->a_colptr;
+    for (int64_t q = 0; q < nj; ++q) {
+      at_p[q] = cs->a_colent[q];
+      at_row[q] = static_cast<int32_t>(jr[at_p[q]]);
+    }
+  } else {
+    atptr.assign(n + 1, 0);
+    for (int64_t p = 0; p < nj; ++p) atptr[jc[p] + 1]++;
+    for (int64_t j = 0; j < n; ++j) atptr[j + 1] += atptr[j];
     std::vector<int64_t> fl(atptr.begin(), atptr.end() - 1);
     for (int64_t p = 0; p < nj; ++p) {
       int64_t q = fl[jc[p]]++;
