@@ -187,20 +187,40 @@ static void condense(Condense &C, int64_t n, int64_t nh, const int64_t *hr, cons
   for (int64_t t = 0; t < nh; ++t) bad |= !(hc[t] <= hr[t] && hr[t] >= 0 && hr[t] < n && hc[t] >= 0);
   GN_REQUIRE(!bad, "Hessian entry out of range or above the diagonal");
   // Jacobian row segments and their product offsets (np.tril_indices order)
-  C.seg.clear();
-  C.seg_row.clear();
-  std::vector<int32_t> pseg(nj);
-  for (int64_t st = 0; st < nj;) {
-    int64_t en = st;
-    while (en < nj && jr[en] == jr[st]) ++en;
-    for (int64_t e = st; e < en; ++e) pseg[e] = static_cast<int32_t>(C.seg.size());
-    C.seg.push_back(st);
-    C.seg_row.push_back(jr[st]);
-    st = en;
+  // (parallel: segment starts, a blocked prefix count, then the placement)
+  uvec<int32_t> pseg(nj);
+  int64_t nseg = 0;
+  {
+    const int nt = std::max(1, std::min(omp_get_max_threads(), static_cast<int>(nj / 65536 + 1)));
+    std::vector<int64_t> cnt(nt + 1, 0);
+#pragma omp parallel num_threads(nt)
+    {
+      const int t = omp_get_thread_num();
+      const int64_t lo = nj * t / nt, hi = nj * (t + 1) / nt;
+      int64_t c = 0;
+      for (int64_t e = lo; e < hi; ++e) c += (e == 0 || jr[e] != jr[e - 1]);
+      cnt[t + 1] = c;
+#pragma omp barrier
+#pragma omp single
+      for (int q = 0; q < nt; ++q) cnt[q + 1] += cnt[q];
+      int64_t g = cnt[t] - 1;
+      for (int64_t e = lo; e < hi; ++e) {
+        g += (e == 0 || jr[e] != jr[e - 1]);
+        pseg[e] = static_cast<int32_t>(g);
+      }
+    }
+    nseg = cnt[nt];
   }
-  const int64_t nseg = static_cast<int64_t>(C.seg.size());
-  C.seg.push_back(nj);
-  C.seg_row.push_back(-1);
+  C.seg.resize(nseg + 1);
+  C.seg_row.resize(nseg + 1);
+#pragma omp parallel for schedule(static)
+  for (int64_t e = 0; e < nj; ++e)
+    if (e == 0 || jr[e] != jr[e - 1]) {
+      C.seg[pseg[e]] = e;
+      C.seg_row[pseg[e]] = jr[e];
+    }
+  C.seg[nseg] = nj;
+  C.seg_row[nseg] = -1;
   C.seg_poff.assign(nseg + 1, 0);
   for (int64_t g = 0; g < nseg; ++g) {
     const int64_t k = C.seg[g + 1] - C.seg[g];
