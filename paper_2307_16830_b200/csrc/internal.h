@@ -252,6 +252,10 @@ struct Symbolic {
   int64_t front_doubles = 0, vec_doubles = 0, max_front = 0, max_cols = 0, n_levels = 0;
   int64_t flops = 0;
   long long *trace = nullptr;   // optional device [3][nf][4] timing stamps
+  // the large-front kernels run on `aux`, forked after the counter reset and
+  // joined before the caller's next work, so they overlap the small-front
+  // kernel of the same sweep (their fronts wait on dependency counters)
+  void *aux = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
   int64_t counters_cap = 0;     // instances the dependency-counter array holds
   // device
   bool uploaded = false;
