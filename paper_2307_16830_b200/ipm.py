@@ -244,6 +244,10 @@ class _DeviceSolve:
         self.host = self.host_mail[:96]
         self.host_flags = self.host_mail[96:].view(torch.int32)
         self.stream = torch.cuda.current_stream()
+        # the Newton right-hand side (independent of the factorisation) is
+        # built on a second stream while the speculative factorisation runs
+        self.aux = torch.cuda.Stream(device=dev)
+        self.ev_prep, self.ev_rhs = torch.cuda.Event(), torch.cuda.Event()
         # frozen gradient scaling at x0 (ipm.py:179-193), relax_equalities on
         # the scaled ranges (ipm.py:112-123), the start point and the unit
         # bound duals, all on the device (gn_ipm_setup); the flags of the
@@ -498,6 +502,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         with span("prep"):
             L.check(lib.gn_ipm_prep(ws.handle, ctypes.byref(V), len(cands), mus, L.ptr(P.scal),
                                     stream))
+        P.ev_prep.record(P.stream)
         return P.read_async(0, 49), cands
 
     pending = launch_eval_prep(state["mu"]) if opts.max_iter > 0 else None
@@ -557,14 +562,22 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
         # ---- Newton step (ipm.py:434-453)
         pv = pv_buf          # overwritten in full by gn_ipm_pvec
         pvc = pv.c_struct()
-        L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), stream))
+        # right-hand side and its condensation on the second stream, after
+        # the prep (which precedes the factorisation on the solver's stream):
+        # they run beside the factorisation; the solve waits for them
+        with torch.cuda.stream(P.aux):
+            P.aux.wait_event(P.ev_prep)
+            L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), P.aux.cuda_stream))
+            cond = ws._condense(pv, "main")
+            P.ev_rhs.record(P.aux)
+        P.stream.wait_event(P.ev_rhs)
         t0 = t_lin
         try:
             # the speculative factorisation above is used without reading the
             # pivot flag; it comes back with the first refinement read, and
             # only a failure falls back to the regularisation schedule of
             # solve_with_regularization (kkt.py:424-447)
-            dx, ds, dy = backend.solve_pvec(pv, "main")
+            dx, ds, dy = backend.solve_condensed(cond, "main")
             delta_w = 0.0
             steps = assemble_steps(ws, pv, dx, ds, dy, check=False, slot="main")
             try:

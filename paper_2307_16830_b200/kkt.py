@@ -524,6 +524,17 @@ class CondensedBackend:
             ds, dy = ws.recover_slack_dual(dx, qx, qs, qy, slot)
         return dx, ds, dy
 
+    def solve_condensed(self, cond, slot=None):
+        """solve_pvec's solve and recovery for a right-hand side condensed
+        beforehand (`cond` = ws._condense(pv, slot), e.g. on another stream)."""
+        ws = self.ws
+        qx, qs, qy, rhs = cond
+        with span("solve"):
+            dx = S.solve_device(self.factor, rhs, D.empty(ws.n) if slot is None else ws._buf(("dx", slot), ws.n))
+        with span("recover"):
+            ds, dy = ws.recover_slack_dual(dx, qx, qs, qy, slot)
+        return dx, ds, dy
+
 
 def solve_with_regularization(ws, backend, pv: PVec, reg: RegState, slot=None):
     """Factorize with the inertia-correction schedule, then solve (kkt.py:424-447)."""
