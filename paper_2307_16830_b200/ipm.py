@@ -569,6 +569,7 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             P.aux.wait_event(P.ev_prep)
             L.check(lib.gn_ipm_pvec(ws.handle, ctypes.byref(V), mu, ctypes.byref(pvc), P.aux.cuda_stream))
             cond = ws._condense(pv, "main")
+            ws.matrix_scale_device(ws._scal[2:3])   # the refinement's scale (delta_w = delta_c = 0)
             P.ev_rhs.record(P.aux)
         P.stream.wait_event(P.ev_rhs)
         t0 = t_lin
@@ -581,7 +582,8 @@ def solve(model, options: SolverOptions | None = None, constraint_ranges=None) -
             delta_w = 0.0
             steps = assemble_steps(ws, pv, dx, ds, dy, check=False, slot="main")
             try:
-                ir = iterative_refinement(ws, backend, steps, pv, check_factor=backend.fws.fail)
+                ir = iterative_refinement(ws, backend, steps, pv, check_factor=backend.fws.fail,
+                                          scale_ready=True)
             except FactorizationFailed:
                 (dx, ds, dy), delta_w = solve_with_regularization(ws, backend, pv, reg, "main")
                 steps = assemble_steps(ws, pv, dx, ds, dy, check=False, slot="main")

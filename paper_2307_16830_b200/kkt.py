@@ -602,7 +602,8 @@ class FactorizationFailed(RuntimeError):
     factorisation behind ``steps`` was not positive definite."""
 
 
-def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None) -> RefinementStats:
+def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None,
+                         scale_ready=False) -> RefinementStats:
     """Refine against the full seven-block system in place (kkt.py:467-491).
 
     The matrix scale and the first residual norm come back in one read;
@@ -610,7 +611,8 @@ def iterative_refinement(ws, backend, steps: Steps, pv: PVec, check_factor=None)
     success was not checked yet) rides along in the same read.
     """
     scal = ws._scal
-    ws.matrix_scale_device(scal[2:3])
+    if not scale_ready:   # (the caller may have queued it already, for the same delta_w / delta_c)
+        ws.matrix_scale_device(scal[2:3])
     res = ws.residual_full(steps, pv, norm_out=scal[0:2], reuse=True)
     if check_factor is not None:
         scal[3:4].copy_(check_factor)
