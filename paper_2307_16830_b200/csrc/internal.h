@@ -256,6 +256,7 @@ struct Symbolic {
   // joined before the caller's next work, so they overlap the small-front
   // kernel of the same sweep (their fronts wait on dependency counters)
   void *aux = nullptr, *ev_fork = nullptr, *ev_join = nullptr;
+  void *aux2 = nullptr, *ev_join2 = nullptr;   // the top-front factor kernel
   int64_t counters_cap = 0;     // instances the dependency-counter array holds
   // device
   bool uploaded = false;
