@@ -286,16 +286,84 @@ struct GatherArgs {
   const double *scal_b;
 };
 
-__global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contrib, int32_t *flags) {
-  int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+// Objective: the flattened contribution list (block order) in contiguous
+// chunks, one CTA each; fixed-order tree sum per CTA, then the last CTA to
+// finish adds the CTA partials in order (deterministic, no FP atomics).
+// These CTAs lead the gather launch (one launch for everything after the
+// pattern kernels).
+constexpr int kGatherThreads = 256;
+constexpr int kObjMaxCtas = 128;
+struct ObjArgs {
+  const int32_t *src;
+  int64_t total;
+  double scale;
+  double *f;
+  double *partials;
+  unsigned *counter;
+  int64_t f_stride;
+  const double *scale_b;
+  int nctas;   // leading CTAs of the launch that reduce the objective (0: none)
+};
+
+__device__ __forceinline__ void objective_cta(const ObjArgs &ob, const double *__restrict__ contrib, int32_t *flags) {
+  __shared__ double red[kGatherThreads];
+  __shared__ bool last;
+  const int64_t bi = blockIdx.y;
+  const unsigned cta = blockIdx.x, nct = static_cast<unsigned>(ob.nctas);
+  double *partials = ob.partials + bi * kObjMaxCtas;
+  unsigned *counter = ob.counter + bi;
+  double *f = ob.f + bi * ob.f_stride;
+  const double scale = ob.scale_b ? ob.scale_b[bi] : ob.scale;
+  const int64_t per = (ob.total + nct - 1) / nct;
+  const int64_t lo = per * cta, hi = min(ob.total, lo + per);
+  double part = 0.0;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += 4 * kGatherThreads) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t q = p + u * kGatherThreads;
+      v[u] = q < hi ? contrib[__ldg(ob.src + q)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) part += v[u];
+  }
+  red[threadIdx.x] = part;
+  __syncthreads();
+  for (int w = kGatherThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[cta] = red[0];
+    __threadfence();
+    last = atomicAdd(counter, 1u) == nct - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double total_sum = 0.0;
+    for (unsigned b = 0; b < nct; ++b) total_sum += __ldcg(partials + b);
+    if (!isfinite(total_sum)) atomicOr(flags, GN_AD_F);
+    *f = total_sum * scale;
+    *counter = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kGatherThreads)
+ad_gather_kernel(GatherArgs ga, ObjArgs ob, const double *__restrict__ contrib, int32_t *flags) {
+  const int64_t bi = blockIdx.y;
+  contrib += bi * ga.contrib_stride;
+  flags += bi;
+  if (static_cast<int>(blockIdx.x) < ob.nctas) {
+    objective_cta(ob, contrib, flags);
+    return;
+  }
+  int64_t t = static_cast<int64_t>(blockIdx.x - ob.nctas) * blockDim.x + threadIdx.x;
   if (t >= ga.begin[ga.nseg]) return;
   int s = 0;
   while (t >= ga.begin[s + 1]) ++s;
   const GatherSeg &G = ga.seg[s];
   int64_t o = t - ga.begin[s];
-  const int64_t bi = blockIdx.y;
-  contrib += bi * ga.contrib_stride;
-  flags += bi;
   double acc = 0.0;
   const int64_t p1 = G.ptr[o + 1];
   for (int64_t p = G.ptr[o]; p < p1; p += 4) {   // four terms' loads in flight, same order
@@ -316,68 +384,6 @@ __global__ void ad_gather_kernel(GatherArgs ga, const double *__restrict__ contr
   else if (G.mode == 2 && scale) sc = scale[o];
   else if (G.mode == 3 && scale) sc = scale[G.rows[o]];
   G.out[bi * G.n_out + o] = G.mode == 0 ? acc : acc * sc;
-}
-
-// non-finite check of directly written outputs (the gather does it otherwise)
-__global__ void finite_check_kernel(int64_t n, const double *__restrict__ v, int32_t *flags, int32_t bit) {
-  int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  v += static_cast<int64_t>(blockIdx.y) * n;   // instance batches: [B][n] values, [B] flags
-  bool bad = t < n && !isfinite(v[t]);
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags + blockIdx.y, bit);
-}
-
-// Objective: the flattened contribution list (block order) in contiguous
-// chunks, one CTA each; fixed-order tree sum per CTA, then the last CTA to
-// finish adds the CTA partials in order (deterministic, no FP atomics).
-constexpr int kObjThreads = 256;
-constexpr int kObjMaxCtas = 128;
-__global__ void __launch_bounds__(kObjThreads)
-ad_objective_kernel(const int32_t *__restrict__ src, int64_t total, const double *__restrict__ contrib,
-                    double scale, double *f, int32_t *flags, double *partials, unsigned *counter,
-                    int64_t contrib_stride, int64_t f_stride, const double *scale_b) {
-  __shared__ double red[kObjThreads];
-  __shared__ bool last;
-  // instance batches (blockIdx.y): own contributions, partials, counter, output
-  const int64_t bi = blockIdx.y;
-  contrib += bi * contrib_stride;
-  partials += bi * kObjMaxCtas;
-  counter += bi;
-  flags += bi;
-  f += bi * f_stride;
-  if (scale_b) scale = scale_b[bi];
-  const int64_t per = (total + gridDim.x - 1) / gridDim.x;
-  const int64_t lo = per * blockIdx.x, hi = min(total, lo + per);
-  double part = 0.0;
-  for (int64_t p = lo + threadIdx.x; p < hi; p += 4 * kObjThreads) {
-    double v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t q = p + u * kObjThreads;
-      v[u] = q < hi ? contrib[__ldg(src + q)] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) part += v[u];
-  }
-  red[threadIdx.x] = part;
-  __syncthreads();
-  for (int w = kObjThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = red[0];
-    __threadfence();
-    last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double total_sum = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) total_sum += __ldcg(partials + b);
-    if (!isfinite(total_sum)) atomicOr(flags, GN_AD_F);
-    *f = total_sum * scale;
-    *counter = 0u;
-  }
 }
 
 }  // namespace
@@ -600,8 +606,9 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
       }
       bs_use = M.d.bstrides_shared;
     }
+    int32_t *fl = flags;
     void *args[] = {&blk, &nblk, &vi, &pa, &tg, &x, &y, &con_scale, &obj_w, &w, &contrib, &jsl, &jac_out, &jdirect,
-                    &bs_use, &objw_b};
+                    &bs_use, &objw_b, &fl};
     GN_REQUIRE(launch_patterns(M.pattern_fn, static_cast<unsigned>(M.n_ctas_rec), st, args,
                                static_cast<unsigned>(B)),
                "pattern kernel launch failed");
@@ -633,30 +640,28 @@ static void ad_eval(Model &M, const double *x, const double *y, double obj_w, co
   if ((what & GN_AD_JAC) && !(M.pattern_fn && M.jac_direct))
     add(static_cast<int64_t>(M.jac_rows.size()), M.d.jac_ptr, M.d.jac_src, jac, con_scale ? 3 : 0, 1.0,
         con_scale, M.d.jac_rows, GN_AD_JAC);
-  if ((what & GN_AD_JAC) && M.pattern_fn && M.jac_direct && !M.jac_rows.empty()) {
-    const int64_t nj = static_cast<int64_t>(M.jac_rows.size());
-    GN_LAUNCH(finite_check_kernel, dim3(static_cast<unsigned>((nj + 255) / 256), B), 256, 0, st, nj, jac, flags,
-              GN_AD_JAC);
-  }
+  // directly written J: the pattern kernels flag non-finite values themselves
   if (what & GN_AD_HESS)
     add(static_cast<int64_t>(M.hess_rows.size()), M.d.hess_ptr, M.d.hess_src, hess, 0, 1.0, nullptr, nullptr, GN_AD_HESS);
   ga.nseg = ns;
-  if (ns > 0) {
-    int64_t tot = ga.begin[ns];
-    GN_LAUNCH(ad_gather_kernel, dim3(static_cast<unsigned>((tot + 255) / 256), B), 256, 0, st, ga, contrib, flags);
-    GN_LAUNCH_CHECK();
-  }
+  ObjArgs ob{};
   if (what & GN_AD_F) {
     const int64_t total = static_cast<int64_t>(M.obj_src.size());
     if (total > 0) {
-      const int g = static_cast<int>(std::min<int64_t>(kObjMaxCtas, (total + 4095) / 4096));
-      GN_LAUNCH(ad_objective_kernel, dim3(g, B), kObjThreads, 0, st, M.d.obj_src, total, contrib, obj_scale, f,
-                flags, M.d.obj_partials, M.d.obj_counter, M.n_contrib, f_stride, objs_b);
+      ob = ObjArgs{M.d.obj_src, total, obj_scale, f, M.d.obj_partials, M.d.obj_counter, f_stride, objs_b,
+                   static_cast<int>(std::min<int64_t>(kObjMaxCtas, (total + 4095) / 4096))};
     } else if (B == 1) {
       GN_CUDA(cudaMemsetAsync(f, 0, sizeof(double), st));
     } else {
       GN_CUDA(cudaMemset2DAsync(f, sizeof(double) * f_stride, 0, sizeof(double), B, st));
     }
+  }
+  const int64_t tot = ns > 0 ? ga.begin[ns] : 0;
+  const int64_t ctas = ob.nctas + (tot + kGatherThreads - 1) / kGatherThreads;
+  if (ctas > 0) {
+    GN_LAUNCH(ad_gather_kernel, dim3(static_cast<unsigned>(ctas), B), kGatherThreads, 0, st, ga, ob, contrib,
+              flags);
+    GN_LAUNCH_CHECK();
   }
 }
 

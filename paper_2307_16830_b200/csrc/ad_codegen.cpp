@@ -104,7 +104,7 @@ std::string gen_pattern(const Model::HBlock &b, int id) {
     << "(long long r, long long R, const int *__restrict__ vi, const double *__restrict__ pa, "
        "const int *__restrict__ tg, const double *__restrict__ x, const double *__restrict__ y, "
        "const double *__restrict__ cs, double obj_w, unsigned what, double *__restrict__ out, "
-       "const int *__restrict__ js, double *__restrict__ jac, int jdirect) {\n";
+       "const int *__restrict__ js, double *__restrict__ jac, int jdirect, int *__restrict__ flags) {\n";
   // record data: coalesced SoA loads of the variable indices and parameters
   std::set<int> vs, ps;
   for (int i = 0; i < T; ++i) {
@@ -166,12 +166,15 @@ std::string gen_pattern(const Model::HBlock &b, int id) {
   if (!obj) {
     // every Jacobian slot has exactly one contributor (checked at upload):
     // write the scaled value straight into J, no contribution round trip
-    o << "      if (jdirect) {\n        const double jsc = cs ? cs[__ldg(tg + r)] : 1.0;\n";
+    // the non-finite check of J rides along (no separate pass over J)
+    o << "      if (jdirect) {\n        const double jsc = cs ? cs[__ldg(tg + r)] : 1.0;\n"
+         "        bool jbad = false;\n";
     for (int k = 0; k < nfirst; ++k) {
       const int s = b.first[k];
-      o << "        jac[__ldg(js + " << k << " * R + r)] = "
-        << (g.has(s) ? "g" + std::to_string(s) : std::string("0.0")) << " * jsc;\n";
+      o << "        { const double jv = " << (g.has(s) ? "g" + std::to_string(s) : std::string("0.0"))
+        << " * jsc; jbad |= !isfinite(jv); jac[__ldg(js + " << k << " * R + r)] = jv; }\n";
     }
+    o << "        if (jbad) atomicOr(flags, " << GN_AD_JAC << ");\n";
     o << "      } else {\n";
   }
   for (int k = 0; k < nfirst; ++k) {
@@ -390,7 +393,7 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
        "const double *__restrict__ params, const int *__restrict__ targets, const double *__restrict__ x, "
        "const double *__restrict__ y, const double *__restrict__ cs, double obj_w, unsigned what, "
        "double *__restrict__ contrib, const int *__restrict__ jslots, double *__restrict__ jac, int jdirect,\n"
-       "    const long long *__restrict__ bs, const double *__restrict__ objw_b) {\n"
+       "    const long long *__restrict__ bs, const double *__restrict__ objw_b, int *__restrict__ flags) {\n"
        "  // instance batches: blockIdx.y = instance, bs = strides (x, y and con_scale, contrib, params, jac)\n"
        "  if (bs) {\n"
        "    const long long bi = blockIdx.y;\n"
@@ -401,6 +404,7 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
        "    params += bi * bs[3];\n"
        "    if (jac) jac += bi * bs[4];\n"
        "    if (objw_b) obj_w = objw_b[bi];\n"
+       "    flags += bi;\n"
        "  }\n"
        "  int lo = 0, hi = nblk - 1;\n"
        "  while (lo < hi) {\n"
@@ -417,7 +421,7 @@ std::string pattern_source(const Model &M, std::vector<int> &pattern_of) {
        "  const int *js = B.jslot_off >= 0 ? jslots + B.jslot_off : jslots;\n"
        "  switch (B.pattern) {\n";
   for (size_t id = 0; id < bodies.size(); ++id)
-    o << "    case " << id << ": pat_" << id << "(r, B.R, vi, pa, tg, x, y, cs, obj_w, what, out, js, jac, jdirect); break;\n";
+    o << "    case " << id << ": pat_" << id << "(r, B.R, vi, pa, tg, x, y, cs, obj_w, what, out, js, jac, jdirect, flags); break;\n";
   o << "    default: break;\n  }\n}\n";
   return o.str();
 }
