@@ -356,7 +356,7 @@ int gn_ipm_setup(int64_t n, int64_t m, int64_t nj, const double *g0, const doubl
  * (midpoint of [sl, su] where that interval is empty) and theta = sum |g - s|.
  * red_partials: GN_RED_PARTIALS doubles; red_counter: one zeroed uint32 (left
  * zeroed). */
-#define GN_RED_PARTIALS (296 * 40)
+#define GN_RED_PARTIALS (1184 * 40)
 int gn_ipm_init_slacks(int64_t m, const double *g, const double *sl, const double *su, double push_tol,
                        double *s, double *theta, double *red_partials, uint32_t *red_counter, void *stream);
 

@@ -49,7 +49,7 @@ class IpmVecs(ctypes.Structure):
 IPM_MAX_MU = 16
 PREP_S = 24
 PREP_DOUBLES = 48
-GN_RED_PARTIALS = 296 * 40   # gridopf.h: reduction scratch of gn_ipm_init_slacks
+GN_RED_PARTIALS = 1184 * 40   # gridopf.h: reduction scratch of gn_ipm_init_slacks
 
 
 class GridOpfError(RuntimeError):

@@ -12,8 +12,11 @@ namespace gn {
 enum RedOp : int { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
 
 constexpr int kRedThreads = 256;
-constexpr int kRedMaxBlocks = 296;   // 2 CTAs per SM on 148 SMs
+// 8 CTAs per SM on 148 SMs: the fused IPM kernels gather (Aᵀy, A·dx) per
+// element, so memory-level parallelism, not the partials, sets their time
+constexpr int kRedMaxBlocks = 1184;
 constexpr int kRedMaxSlots = 40;
+static_assert(GN_RED_PARTIALS == kRedMaxBlocks * kRedMaxSlots, "gridopf.h GN_RED_PARTIALS out of date");
 
 // Batched launches reduce every instance (blockIdx.y) separately: its CTA
 // partials at partials + (y * gridDim.x + blockIdx.x) * kRedMaxSlots, its
@@ -85,8 +88,17 @@ __device__ void grid_reduce(const RedSpec &spec, double (&vals)[K]) {
   for (int k = warp; k < spec.k; k += nw) {   // one warp per slot over the CTA partials
     const int op = spec.op[k];
     double v = red_identity(op);
-    for (unsigned b = lane; b < gridDim.x; b += 32)
-      v = red_combine(op, v, __ldcg(partials + b * kRedMaxSlots + k));
+    for (unsigned b0 = lane; b0 < gridDim.x; b0 += 32 * 8) {   // 8 loads in flight, same order
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const unsigned b = b0 + 32u * u;
+        t[u] = b < gridDim.x ? __ldcg(partials + b * kRedMaxSlots + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b0 + 32u * u < gridDim.x) v = red_combine(op, v, t[u]);
+    }
     for (int o = 16; o > 0; o >>= 1) v = red_combine(op, v, __shfl_down_sync(0xffffffffu, v, o));
     if (lane == 0) out[k] = v;
   }
