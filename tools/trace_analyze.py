@@ -33,7 +33,22 @@ def analyse(path):
             print(f"  {lab:5s} n={mk.sum():6d} end {np.nanmax(t[mk, 3]) / 1e3:8.1f} us  "
                   f"work mean {np.nanmean(dur) / 1e3:7.2f} us max {np.nanmax(dur) / 1e3:7.1f}  "
                   f"wait mean {np.nanmean(wait) / 1e3:7.2f} us  sum work {np.nansum(dur) / 1e3:9.0f} us")
-        if ph == 0:
+        if ph == 2:
+            # backward: the last-finishing front and its chain of parents
+            J = int(np.nanargmax(t[:, 3]))
+            chain = []
+            while J >= 0 and J < len(parent):
+                chain.append(J)
+                pj = int(parent[J])
+                if pj == J or pj < 0:
+                    break
+                J = pj
+            print("  backward critical chain (last front first): front w s  start, wait, work us")
+            for J in chain[:60]:
+                a = t[J]
+                print(f"   {J:6d} w={ncols[J]:4d} s={nrows[J]:4d} {'S' if small[J] else 'L'} "
+                      f"start {a[0] / 1e3:8.1f} wait {(a[1] - a[0]) / 1e3:7.1f} work {(a[3] - a[1]) / 1e3:7.1f}")
+        if ph in (0, 1):
             # critical path backwards from the last-finishing root
             J = int(np.nanargmax(t[:, 3]))
             chain = []
@@ -48,7 +63,7 @@ def analyse(path):
                 J = max(ch, key=lambda c: t[c, 3])
             tot = 0.0
             print("  critical chain (root first): front w s  [wait->deps, deps->asm, asm->done] us")
-            if "panels" in d:
+            if ph == 0 and "panels" in d:
                 pt = d["panels"].astype(np.float64)[:32]
                 ok = pt[:, 0] > 0
                 if ok.any():
