@@ -639,9 +639,9 @@ def main():
     secondary = phase_rooflines(model, ws, info, phases, peak, dmma_peak)
 
     # DRAM traffic of one refactorisation from the committed ncu capture of
-    # the same kernels (profiles/, tools/profile_round.sh), C3 only
+    # the same kernels (profiles/, tools/gpu_r2y.sh), C3 only
     traffic = None
-    tpath = os.path.join(HERE, "profiles", "r01e_traffic_C3.json")
+    tpath = os.path.join(HERE, "profiles", "r02y_traffic_C3.json")
     if args.workload == "C3" and os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get("refactor_bytes_per_launch")
@@ -680,7 +680,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "refactorisation (mf_factor_small + mf_factor_large + mf_factor_top)",
                      "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": traffic, "traffic_source": "profiles/r01e_traffic_C3.json (ncu, cold L2)",
+                     "traffic": traffic, "traffic_source": "profiles/r02y_traffic_C3.json (ncu, cold L2)",
                      "alg_bytes_per_launch": alg_bytes,
                      "mean_launch_ms": ref["mean_ms"]},
         "rooflines_secondary": secondary,
