@@ -205,7 +205,7 @@ struct Condense {
 inline int64_t front_ld(int64_t s) { return s + (s & 1); }
 
 constexpr int kWarpFrontRows = 32;   // fronts this small are factored by one warp
-constexpr int kTopFronts = 24;       // at most this many top fronts go to the cluster kernel
+constexpr int kTopFronts = 96;       // at most this many top fronts go to the cluster kernel
 constexpr int kTopMinRows = 96;      // ... and only fronts at least this tall
 
 // device record of one front (loaded with four 16-byte loads)
